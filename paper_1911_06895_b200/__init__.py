@@ -1,4 +1,46 @@
-"""B200-native drop-in for the reference's delta-stepping SSSP path."""
+"""B200-native drop-in for the reference's delta-stepping SSSP path.
+
+Public names follow the reference package `deltasparse` for this path
+(/root/reference/pkg/src/deltasparse/__init__.py): `delta_stepping`,
+`SsspResult`, `split_edges`, `BackendChoice`, `bucket_bounds`, the
+`SparseMatrix` / `SparseVector` containers and their builders.  Compute runs
+in libdsssp.so (sm_100a) through the C-ABI declared in include/dsssp.h.
+"""
+
 from .containers import (  # noqa: F401
-    SparseMatrix, SparseVector, mask_from_indices, matrix_build, vector_build,
+    SparseMatrix,
+    SparseVector,
+    mask_from_indices,
+    matrix_build,
+    vector_build,
 )
+from .graphs import random_connected_unit_graph, random_graph  # noqa: F401
+from .sssp import (  # noqa: F401
+    BackendChoice,
+    DeviceGraph,
+    SsspResult,
+    bucket_bounds,
+    clear_device_cache,
+    delta_stepping,
+    split_edges,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "SparseMatrix",
+    "SparseVector",
+    "mask_from_indices",
+    "matrix_build",
+    "vector_build",
+    "random_graph",
+    "random_connected_unit_graph",
+    "BackendChoice",
+    "DeviceGraph",
+    "SsspResult",
+    "bucket_bounds",
+    "clear_device_cache",
+    "delta_stepping",
+    "split_edges",
+    "__version__",
+]

@@ -1,0 +1,123 @@
+"""ctypes binding of libdsssp.so (include/dsssp.h).
+
+This is the product path's only route to the device: there is no CPU
+fallback.  If the library is missing, `lib()` raises ImportError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .build import LIB
+
+DS_OK, DS_EINVAL, DS_ENOCONVERGE, DS_ECUDA, DS_ENOMEM, DS_ETIMEOUT = 0, 1, 2, 3, 4, 5
+DS_IDX_I32, DS_IDX_I64 = 0, 1
+DS_W_F32, DS_W_F64, DS_W_I32 = 0, 1, 2
+DS_FLAG_SKIP_EMPTY, DS_FLAG_FORCE_F64 = 1, 2
+DS_MODE_FIXED32, DS_MODE_F64 = 0, 1
+
+# Every entry point include/dsssp.h declares (checked by the CPU tests).
+EXPORTS = (
+    "ds_graph_create", "ds_graph_prepare", "ds_sssp", "ds_result_dense", "ds_result_sparse",
+    "ds_export_split", "ds_graph_set_stream", "ds_graph_size", "ds_graph_destroy",
+    "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download",
+)
+
+
+class PrepInfo(ctypes.Structure):
+    _fields_ = [
+        ("nnz_light", ctypes.c_int64),
+        ("nnz_heavy", ctypes.c_int64),
+        ("min_light_weight", ctypes.c_double),
+        ("phase_ceiling", ctypes.c_int64),
+        ("dist_mode", ctypes.c_int32),
+        ("frac_bits", ctypes.c_int32),
+        ("prepare_ms", ctypes.c_double),
+    ]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("outer_iterations", ctypes.c_int64),
+        ("inner_phases", ctypes.c_int64),
+        ("buckets_visited", ctypes.c_int64),
+        ("reached", ctypes.c_int64),
+        ("edges_reached", ctypes.c_int64),
+        ("edges_scanned", ctypes.c_int64),
+        ("grid_barriers", ctypes.c_int64),
+        ("max_distance", ctypes.c_double),
+        ("kernel_ms", ctypes.c_double),
+        ("dist_mode", ctypes.c_int32),
+        ("fallbacks", ctypes.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class DsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+_lib = None
+_lock = threading.Lock()
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+def lib():
+    """Load libdsssp.so once; raise ImportError if it was never built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB):
+            raise ImportError(
+                f"{LIB} is missing: build it with `python -m paper_1911_06895_b200.build` "
+                "(the solver has no CPU fallback)")
+        L = ctypes.CDLL(LIB)
+        L.ds_graph_create.argtypes = [_i64, _i64, _vp, _vp, ctypes.c_int, _vp, ctypes.c_int,
+                                      ctypes.c_int, _vp, ctypes.POINTER(_vp)]
+        L.ds_graph_prepare.argtypes = [_vp, ctypes.c_double, ctypes.c_uint32,
+                                       ctypes.POINTER(PrepInfo)]
+        L.ds_sssp.argtypes = [_vp, _i64, ctypes.c_double, ctypes.c_uint32, ctypes.POINTER(Stats)]
+        L.ds_result_dense.argtypes = [_vp, _vp]
+        L.ds_result_sparse.argtypes = [_vp, _vp, _vp]
+        L.ds_export_split.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp]
+        L.ds_graph_set_stream.argtypes = [_vp, _vp]
+        L.ds_graph_size.argtypes = [_vp, _i64p, _i64p]
+        L.ds_graph_destroy.argtypes = [_vp]
+        L.ds_graph_destroy.restype = None
+        L.ds_last_error.restype = ctypes.c_char_p
+        L.ds_device_count.restype = ctypes.c_int
+        L.ds_gen_rmat.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
+                                  ctypes.c_uint64, ctypes.c_int, _vp, ctypes.POINTER(_vp)]
+        L.ds_graph_download.argtypes = [_vp, _vp, _vp, _vp]
+        for name in ("ds_graph_create", "ds_graph_prepare", "ds_sssp", "ds_result_dense",
+                     "ds_result_sparse", "ds_export_split", "ds_graph_set_stream",
+                     "ds_graph_size", "ds_gen_rmat", "ds_graph_download"):
+            getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Map a DS_* return code onto the reference's exception types."""
+    if rc == DS_OK:
+        return
+    msg = lib().ds_last_error().decode(errors="replace")
+    if rc == DS_EINVAL:
+        raise ValueError(msg)
+    raise DsError(rc, msg)
+
+
+def device_count() -> int:
+    return int(lib().ds_device_count())

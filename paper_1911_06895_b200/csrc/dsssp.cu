@@ -1,0 +1,946 @@
+// dsssp.cu -- C-ABI of the sm_100a delta-stepping library (include/dsssp.h).
+//
+// Device graph store: original CSR (int64 offsets, int32 columns, f64
+// weights) plus, per delta, a light and a heavy CSR (split_edges,
+// sssp.py:106-150) in the distance mode's edge layout:
+//   fixed32 : uint2 {col, w * 2^frac}       8 B/edge
+//   f64     : {col, pad, double w}          16 B/edge
+// Per-vertex scratch (distances, stamps, frontier/S lists, capture entries)
+// is allocated once per handle and reused by every solve.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_scan.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/dsssp.h"
+#include "common.cuh"
+#include "sssp_kernel.cuh"
+
+using namespace ds;
+
+// ---------------------------------------------------------------- errors
+
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) {                                                             \
+            return set_err(e_ == cudaErrorMemoryAllocation ? DS_ENOMEM : DS_ECUDA,            \
+                           "CUDA error %s (%s) at %s:%d", cudaGetErrorName(e_),               \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);                       \
+        }                                                                                    \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (cudaGetDevice(&cur) == cudaSuccess && prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// ---------------------------------------------------------------- handle
+
+struct PrepStats {
+    unsigned long long min_light_bits;
+    unsigned long long max_w_bits;
+    int max_frac;
+    int pad;
+    unsigned long long nL, nH;
+};
+
+struct ds_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    long long n = 0, nnz = 0;
+    int nsm = 0;
+    // original CSR
+    long long* indptr = nullptr;
+    int* col = nullptr;
+    double* w = nullptr;
+    // prepared split
+    bool prepared = false;
+    double delta = 0;
+    int mode = DS_MODE_FIXED32;
+    int frac = 0;
+    long long nL = 0, nH = 0;
+    double minL = INFINITY;
+    long long ceiling = 0;
+    double prep_ms = 0;
+    double overflow_delta = NAN;  // delta whose fixed-point solve overflowed
+    long long* Lptr = nullptr;
+    long long* Hptr = nullptr;
+    void* Ledges = nullptr;
+    void* Hedges = nullptr;
+    size_t Lcap = 0, Hcap = 0;
+    // scratch
+    void* dist = nullptr;  // 8n bytes (either mode)
+    unsigned* fstamp = nullptr;
+    unsigned* sstamp = nullptr;
+    int* F0 = nullptr;
+    int* F1 = nullptr;
+    int* S = nullptr;
+    long long* Rpre = nullptr;
+    long long* Rbase = nullptr;
+    void* Rd = nullptr;
+    unsigned* tile_start = nullptr;
+    unsigned long long* tflag = nullptr;
+    unsigned long long* tagg = nullptr;
+    unsigned long long* tinc = nullptr;
+    Ctl* ctl = nullptr;
+    Ctl* h_ctl = nullptr;  // pinned
+    PrepStats* pstat = nullptr;
+    PrepStats* h_pstat = nullptr;
+    double* out = nullptr;
+    long long* cidx = nullptr;
+    unsigned long long* ccount = nullptr;
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    // serials (stamps / look-back flags persist across solves)
+    unsigned pser = 1, bser = 1;
+    unsigned long long sser = 1;
+    // last result
+    bool have_result = false;
+    long long reached = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int grid_fixed = 0, grid_f64 = 0;
+};
+
+static void free_all(ds_graph* g) {
+    void* ptrs[] = {g->indptr, g->col,  g->w,     g->Lptr,  g->Hptr,       g->Ledges, g->Hedges,
+                    g->dist,   g->fstamp, g->sstamp, g->F0,  g->F1,         g->S,      g->Rpre,
+                    g->Rbase,  g->Rd,   g->tile_start, g->tflag, g->tagg,   g->tinc,   g->ctl,
+                    g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (g->h_ctl) cudaFreeHost(g->h_ctl);
+    if (g->h_pstat) cudaFreeHost(g->h_pstat);
+    if (g->ev0) cudaEventDestroy(g->ev0);
+    if (g->ev1) cudaEventDestroy(g->ev1);
+}
+
+static bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static unsigned grid_blocks_for(int nsm, int occ) {
+    int per = std::max(1, std::min(occ, 8));
+    if (const char* s = getenv("DS_BLOCKS_PER_SM")) per = std::max(1, std::min(per, atoi(s)));
+    return (unsigned)(nsm * per);
+}
+
+// ---------------------------------------------------------------- create kernels
+
+__global__ void k_check_indptr(const long long* indptr, long long n, long long nnz, int* bad) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+         r += (long long)gridDim.x * blockDim.x) {
+        const long long a = indptr[r], b = indptr[r + 1];
+        if (a > b || a < 0 || b > nnz) atomicOr(bad, 1);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (indptr[0] != 0 || indptr[n] != nnz))
+        atomicOr(bad, 1);
+}
+
+template <class T>
+__global__ void k_convert_col(const T* in, int* out, long long nnz, long long n, int* bad) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long c = (long long)in[e];
+        if (c < 0 || c >= n) atomicOr(bad, 2);
+        out[e] = (int)c;
+    }
+}
+
+template <class T>
+__global__ void k_convert_w(const T* in, double* out, long long nnz) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+         e += (long long)gridDim.x * blockDim.x)
+        out[e] = (double)in[e];
+}
+
+// ---------------------------------------------------------------- split kernels
+
+// Fraction bits needed to write w (positive, finite) as an integer: w = odd * 2^k.
+__device__ __forceinline__ int frac_bits(double w) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(w);
+    const int ex = (int)((b >> 52) & 0x7FF);
+    unsigned long long m = b & ((1ull << 52) - 1);
+    int e2;
+    if (ex == 0) {
+        e2 = -1074;
+    } else {
+        m |= 1ull << 52;
+        e2 = ex - 1075;
+    }
+    const int low = e2 + (__ffsll((long long)m) - 1);
+    return low < 0 ? -low : 0;
+}
+
+__device__ __forceinline__ bool light_w(double w, double delta) { return w > 0.0 && w <= delta; }
+__device__ __forceinline__ bool heavy_w(double w, double delta) { return w > delta && w < CUDART_INF; }
+
+// warp per row: light/heavy counts, min light weight, fixed-point eligibility
+__global__ void k_split_count(long long n, const long long* indptr, const double* w, double delta,
+                              long long* Lcnt, long long* Hcnt, PrepStats* st) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long minL = ~0ull, maxw = 0, nl = 0, nh = 0;
+    int frac = 0;
+    for (long long r = warp; r < n; r += nwarps) {
+        const long long a = indptr[r], b = indptr[r + 1];
+        unsigned lc = 0, hc = 0;
+        for (long long e = a + lane; e < b; e += 32) {
+            const double x = __ldg(w + e);
+            const bool L = light_w(x, delta), H = heavy_w(x, delta);
+            lc += L;
+            hc += H;
+            if (L || H) {
+                const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+                if (L && bits < minL) minL = bits;
+                if (bits > maxw) maxw = bits;
+                frac = max(frac, frac_bits(x));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            lc += __shfl_xor_sync(0xffffffffu, lc, o);
+            hc += __shfl_xor_sync(0xffffffffu, hc, o);
+        }
+        if (lane == 0) {
+            Lcnt[r] = lc;
+            Hcnt[r] = hc;
+            nl += lc;
+            nh += hc;
+        }
+    }
+    minL = warp_min(minL);
+    maxw = warp_max(maxw);
+    nl = warp_sum(nl);
+    nh = warp_sum(nh);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) frac = max(frac, __shfl_xor_sync(0xffffffffu, frac, o));
+    if (lane == 0) {
+        if (minL != ~0ull) atomicMin(&st->min_light_bits, minL);
+        if (maxw) atomicMax(&st->max_w_bits, maxw);
+        if (frac) atomicMax(&st->max_frac, frac);
+        if (nl) atomicAdd(&st->nL, nl);
+        if (nh) atomicAdd(&st->nH, nh);
+    }
+}
+
+__device__ __forceinline__ void put_edge(uint2* out, long long i, int c, double x, int frac) {
+    out[i] = make_uint2((unsigned)c, (unsigned)ldexp(x, frac));
+}
+__device__ __forceinline__ void put_edge(EdgeF64* out, long long i, int c, double x, int) {
+    EdgeF64 e;
+    e.col = (unsigned)c;
+    e.pad = 0;
+    e.w = x;
+    out[i] = e;
+}
+
+// warp per row: stable partition of the row into A_L / A_H (order preserved,
+// filter_matrix semantics, ops.py:158-176)
+template <class Edge>
+__global__ void k_split_scatter(long long n, const long long* indptr, const int* col,
+                                const double* w, double delta, int frac, const long long* Lptr,
+                                const long long* Hptr, Edge* Lout, Edge* Hout) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (long long r = warp; r < n; r += nwarps) {
+        const long long a = indptr[r], b = indptr[r + 1];
+        long long lb = Lptr[r], hb = Hptr[r];
+        for (long long e0 = a; e0 < b; e0 += 32) {
+            const long long e = e0 + lane;
+            double x = 0;
+            int c = 0;
+            if (e < b) {
+                x = __ldg(w + e);
+                c = __ldg(col + e);
+            }
+            const bool L = e < b && light_w(x, delta);
+            const bool H = e < b && heavy_w(x, delta);
+            const unsigned mL = __ballot_sync(0xffffffffu, L);
+            const unsigned mH = __ballot_sync(0xffffffffu, H);
+            if (L) put_edge(Lout, lb + __popc(mL & lt), c, x, frac);
+            if (H) put_edge(Hout, hb + __popc(mH & lt), c, x, frac);
+            lb += __popc(mL);
+            hb += __popc(mH);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- compaction
+
+constexpr int kCompItems = 16;
+constexpr int kCompTile = kThreads * kCompItems;
+
+__global__ void k_compact_count(const double* d, long long n, unsigned long long* counts) {
+    const long long base = blockIdx.x * (long long)kCompTile + threadIdx.x * kCompItems;
+    unsigned long long c = 0;
+    for (int j = 0; j < kCompItems; ++j) {
+        const long long v = base + j;
+        if (v < n && d[v] != CUDART_INF) ++c;
+    }
+    __shared__ unsigned long long buf[kThreads / 32];
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0) buf[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < kThreads / 32; ++i) t += buf[i];
+        counts[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_compact_write(const double* d, long long n, const unsigned long long* offsets,
+                                long long* idx, double* val) {
+    using Scan = cub::BlockScan<unsigned long long, kThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    const long long base = blockIdx.x * (long long)kCompTile + threadIdx.x * kCompItems;
+    unsigned long long c = 0;
+    for (int j = 0; j < kCompItems; ++j) {
+        const long long v = base + j;
+        if (v < n && d[v] != CUDART_INF) ++c;
+    }
+    unsigned long long ex;
+    Scan(tmp).ExclusiveSum(c, ex);
+    unsigned long long o = offsets[blockIdx.x] + ex;
+    for (int j = 0; j < kCompItems; ++j) {
+        const long long v = base + j;
+        if (v < n) {
+            const double x = d[v];
+            if (x != CUDART_INF) {
+                idx[o] = v;
+                val[o] = x;
+                ++o;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- helpers
+
+static int ensure_cub(ds_graph* g, size_t bytes) {
+    if (bytes <= g->cub_bytes) return DS_OK;
+    if (g->cub_tmp) CK(cudaFree(g->cub_tmp));
+    g->cub_tmp = nullptr;
+    CK(cudaMalloc(&g->cub_tmp, bytes));
+    g->cub_bytes = bytes;
+    return DS_OK;
+}
+
+static int inclusive_scan_i64(ds_graph* g, const long long* in, long long* out, long long count) {
+    size_t bytes = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, bytes, in, out, count, g->stream));
+    int rc = ensure_cub(g, bytes);
+    if (rc) return rc;
+    CK(cub::DeviceScan::InclusiveSum(g->cub_tmp, bytes, in, out, count, g->stream));
+    return DS_OK;
+}
+
+static unsigned elementwise_grid(ds_graph* g) { return (unsigned)(g->nsm * 8); }
+
+// ---------------------------------------------------------------- API
+
+extern "C" const char* ds_last_error(void) { return g_err.c_str(); }
+
+extern "C" int ds_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+extern "C" int ds_graph_set_stream(ds_graph* g, void* stream) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    g->stream = (cudaStream_t)stream;
+    return DS_OK;
+}
+
+extern "C" int ds_graph_size(const ds_graph* g, int64_t* n, int64_t* nnz) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    if (n) *n = g->n;
+    if (nnz) *nnz = g->nnz;
+    return DS_OK;
+}
+
+static int alloc_scratch(ds_graph* g) {
+    const long long n = g->n;
+    CK(cudaMalloc(&g->dist, sizeof(unsigned long long) * n));
+    CK(cudaMalloc(&g->fstamp, sizeof(unsigned) * n));
+    CK(cudaMalloc(&g->sstamp, sizeof(unsigned) * n));
+    CK(cudaMalloc(&g->F0, sizeof(int) * n));
+    CK(cudaMalloc(&g->F1, sizeof(int) * n));
+    CK(cudaMalloc(&g->S, sizeof(int) * n));
+    CK(cudaMalloc(&g->Rpre, sizeof(long long) * n));
+    CK(cudaMalloc(&g->Rbase, sizeof(long long) * n));
+    CK(cudaMalloc(&g->Rd, sizeof(unsigned long long) * n));
+    const long long ntile_rel = g->nnz / kRelTile + 4;
+    CK(cudaMalloc(&g->tile_start, sizeof(unsigned) * ntile_rel));
+    const long long ntile_cap = n / kCapTile + 4;
+    CK(cudaMalloc(&g->tflag, sizeof(unsigned long long) * ntile_cap));
+    CK(cudaMalloc(&g->tagg, 2 * sizeof(unsigned long long) * ntile_cap));
+    CK(cudaMalloc(&g->tinc, 2 * sizeof(unsigned long long) * ntile_cap));
+    CK(cudaMalloc(&g->ctl, sizeof(Ctl)));
+    CK(cudaMallocHost(&g->h_ctl, sizeof(Ctl)));
+    CK(cudaMalloc(&g->pstat, sizeof(PrepStats)));
+    CK(cudaMallocHost(&g->h_pstat, sizeof(PrepStats)));
+    CK(cudaMalloc(&g->out, sizeof(double) * n));
+    CK(cudaMalloc(&g->Lptr, sizeof(long long) * (n + 1)));
+    CK(cudaMalloc(&g->Hptr, sizeof(long long) * (n + 1)));
+    CK(cudaMemsetAsync(g->fstamp, 0, sizeof(unsigned) * n, g->stream));
+    CK(cudaMemsetAsync(g->sstamp, 0, sizeof(unsigned) * n, g->stream));
+    CK(cudaMemsetAsync(g->tflag, 0, sizeof(unsigned long long) * ntile_cap, g->stream));
+    CK(cudaEventCreate(&g->ev0));
+    CK(cudaEventCreate(&g->ev1));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeFixed>,
+                                                     kThreads, 0));
+    g->grid_fixed = (int)grid_blocks_for(g->nsm, occ);
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeF64>,
+                                                     kThreads, 0));
+    g->grid_f64 = (int)grid_blocks_for(g->nsm, occ);
+    if (g->grid_fixed <= 0 || g->grid_f64 <= 0)
+        return set_err(DS_ECUDA, "persistent solver kernel cannot be resident on this device");
+    return DS_OK;
+}
+
+static int graph_init(ds_graph* g, int device, void* stream, long long n, long long nnz) {
+    g->device = device;
+    g->stream = (cudaStream_t)stream;
+    g->n = n;
+    g->nnz = nnz;
+    CK(cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, device));
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+    if (!coop) return set_err(DS_ECUDA, "device %d lacks cooperative launch", device);
+    CK(cudaMalloc(&g->indptr, sizeof(long long) * (n + 1)));
+    CK(cudaMalloc(&g->col, sizeof(int) * std::max(nnz, 1LL)));
+    CK(cudaMalloc(&g->w, sizeof(double) * std::max(nnz, 1LL)));
+    return alloc_scratch(g);
+}
+
+static int check_csr(ds_graph* g) {
+    int* bad = reinterpret_cast<int*>(g->pstat);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
+    k_check_indptr<<<elementwise_grid(g), 256, 0, g->stream>>>(g->indptr, g->n, g->nnz, bad);
+    CK(cudaGetLastError());
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    if (h) return set_err(DS_EINVAL, "indptr must start at 0, be non-decreasing and end at nnz");
+    return DS_OK;
+}
+
+extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, const void* col,
+                               int col_dtype, const void* val, int val_dtype, int device,
+                               void* stream, ds_graph** out) {
+    if (!out) return set_err(DS_EINVAL, "null output handle");
+    *out = nullptr;
+    if (n < 1) return set_err(DS_EINVAL, "matrix dimension must be positive, got %lld", (long long)n);
+    if (n > 0x7FFFFFFFLL) return set_err(DS_EINVAL, "vertex count %lld exceeds int32 ids", (long long)n);
+    if (nnz < 0) return set_err(DS_EINVAL, "negative nnz");
+    if (nnz > 0 && (!indptr || !col || !val)) return set_err(DS_EINVAL, "null CSR array");
+    if (!indptr) return set_err(DS_EINVAL, "null indptr");
+    if (col_dtype != DS_IDX_I32 && col_dtype != DS_IDX_I64)
+        return set_err(DS_EINVAL, "unknown column dtype %d", col_dtype);
+    if (val_dtype != DS_W_F32 && val_dtype != DS_W_F64 && val_dtype != DS_W_I32)
+        return set_err(DS_EINVAL, "unknown weight dtype %d", val_dtype);
+    int ndev = ds_device_count();
+    if (device < 0 || device >= ndev)
+        return set_err(DS_ECUDA, "CUDA device %d not available (%d visible)", device, ndev);
+    DeviceGuard guard(device);
+    ds_graph* g = new ds_graph();
+    int rc = graph_init(g, device, stream, n, nnz);
+    if (rc) {
+        free_all(g);
+        delete g;
+        return rc;
+    }
+    auto fail = [&](int code) {
+        std::string keep = g_err;
+        cudaStreamSynchronize(g->stream);
+        free_all(g);
+        delete g;
+        g_err = keep;
+        return code;
+    };
+#define CKG(call)                                                                          \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(set_err(e_ == cudaErrorMemoryAllocation ? DS_ENOMEM : DS_ECUDA,     \
+                                "CUDA error %s at %s:%d", cudaGetErrorName(e_), __FILE__,  \
+                                __LINE__));                                                \
+    } while (0)
+    const cudaMemcpyKind kind_p = is_device_ptr(indptr) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CKG(cudaMemcpyAsync(g->indptr, indptr, sizeof(long long) * (n + 1), kind_p, g->stream));
+    if ((rc = check_csr(g))) return fail(rc);
+    int* bad = reinterpret_cast<int*>(g->pstat);
+    CKG(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
+    if (nnz > 0) {
+        const unsigned grid = elementwise_grid(g);
+        // columns: straight copy for int32 (range-checked in place), convert int64
+        const size_t csz = col_dtype == DS_IDX_I32 ? 4 : 8;
+        void* stage = nullptr;
+        const bool col_dev = is_device_ptr(col);
+        const void* csrc = col;
+        if (!col_dev || col_dtype == DS_IDX_I32) {
+            if (col_dtype == DS_IDX_I32) {
+                CKG(cudaMemcpyAsync(g->col, col, csz * nnz,
+                                    col_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                    g->stream));
+                csrc = g->col;
+            } else {
+                CKG(cudaMalloc(&stage, csz * nnz));
+                CKG(cudaMemcpyAsync(stage, col, csz * nnz, cudaMemcpyHostToDevice, g->stream));
+                csrc = stage;
+            }
+        }
+        if (col_dtype == DS_IDX_I32)
+            k_convert_col<int><<<grid, 256, 0, g->stream>>>((const int*)csrc, g->col, nnz, n, bad);
+        else
+            k_convert_col<long long><<<grid, 256, 0, g->stream>>>((const long long*)csrc, g->col,
+                                                                   nnz, n, bad);
+        CKG(cudaGetLastError());
+        if (stage) {
+            CKG(cudaStreamSynchronize(g->stream));
+            cudaFree(stage);
+            stage = nullptr;
+        }
+        // weights -> f64
+        const bool val_dev = is_device_ptr(val);
+        if (val_dtype == DS_W_F64) {
+            CKG(cudaMemcpyAsync(g->w, val, 8 * nnz,
+                                val_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->stream));
+        } else {
+            const void* vsrc = val;
+            if (!val_dev) {
+                CKG(cudaMalloc(&stage, 4 * nnz));
+                CKG(cudaMemcpyAsync(stage, val, 4 * nnz, cudaMemcpyHostToDevice, g->stream));
+                vsrc = stage;
+            }
+            if (val_dtype == DS_W_F32)
+                k_convert_w<float><<<grid, 256, 0, g->stream>>>((const float*)vsrc, g->w, nnz);
+            else
+                k_convert_w<int><<<grid, 256, 0, g->stream>>>((const int*)vsrc, g->w, nnz);
+            CKG(cudaGetLastError());
+            if (stage) {
+                CKG(cudaStreamSynchronize(g->stream));
+                cudaFree(stage);
+            }
+        }
+    }
+    int h = 0;
+    CKG(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    CKG(cudaStreamSynchronize(g->stream));
+    if (h & 2) return fail(set_err(DS_EINVAL, "column index out of range for dimension %lld", (long long)n));
+#undef CKG
+    *out = g;
+    return DS_OK;
+}
+
+extern "C" void ds_graph_destroy(ds_graph* g) {
+    if (!g) return;
+    DeviceGuard guard(g->device);
+    cudaStreamSynchronize(g->stream);
+    free_all(g);
+    delete g;
+}
+
+static int ensure_edges(void** buf, size_t* cap, size_t bytes) {
+    bytes = std::max(bytes, (size_t)16);
+    if (bytes <= *cap) return DS_OK;
+    if (*buf) CK(cudaFree(*buf));
+    *buf = nullptr;
+    *cap = 0;
+    CK(cudaMalloc(buf, bytes));
+    *cap = bytes;
+    return DS_OK;
+}
+
+static int prepare(ds_graph* g, double delta, uint32_t flags) {
+    if (!(delta > 0) || !std::isfinite(delta))
+        return set_err(DS_EINVAL, "delta must be a positive finite number, got %g", delta);
+    const bool want_f64 = (flags & DS_FLAG_FORCE_F64) || (delta == g->overflow_delta);
+    if (g->prepared && g->delta == delta && (g->mode == DS_MODE_F64) == want_f64) return DS_OK;
+    g->prepared = false;
+    g->have_result = false;
+    const long long n = g->n;
+    PrepStats init{};
+    init.min_light_bits = ~0ull;
+    *g->h_pstat = init;
+    CK(cudaEventRecord(g->ev0, g->stream));
+    CK(cudaMemcpyAsync(g->pstat, g->h_pstat, sizeof(PrepStats), cudaMemcpyHostToDevice, g->stream));
+    CK(cudaMemsetAsync(g->Lptr, 0, sizeof(long long), g->stream));
+    CK(cudaMemsetAsync(g->Hptr, 0, sizeof(long long), g->stream));
+    // per-row counts into scratch (Rpre / Rbase are n-sized int64)
+    const unsigned grid = (unsigned)(g->nsm * 16);
+    k_split_count<<<grid, 256, 0, g->stream>>>(n, g->indptr, g->w, delta, g->Rpre, g->Rbase, g->pstat);
+    CK(cudaGetLastError());
+    int rc = inclusive_scan_i64(g, g->Rpre, g->Lptr + 1, n);
+    if (rc) return rc;
+    rc = inclusive_scan_i64(g, g->Rbase, g->Hptr + 1, n);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(g->h_pstat, g->pstat, sizeof(PrepStats), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    const PrepStats st = *g->h_pstat;
+    g->nL = (long long)st.nL;
+    g->nH = (long long)st.nH;
+    double minL = INFINITY;
+    if (st.min_light_bits != ~0ull) memcpy(&minL, &st.min_light_bits, 8);
+    double maxw = 0;
+    memcpy(&maxw, &st.max_w_bits, 8);
+    g->minL = minL;
+    // fixed point iff every weight is an integer multiple of 2^-frac and the
+    // largest weight fits well inside 32 bits (runtime overflow is detected)
+    int mode = DS_MODE_F64;
+    int frac = 0;
+    if (!want_f64 && st.max_frac <= 60) {
+        frac = st.max_frac;
+        const double W = ldexp(maxw, frac);
+        if (W < 4294967295.0) mode = DS_MODE_FIXED32;
+    }
+    g->mode = mode;
+    g->frac = mode == DS_MODE_FIXED32 ? frac : 0;
+    // phase ceiling (sssp.py:268-274), saturating
+    long long per = 2;
+    if (g->nL) {
+        const double q = ceil(delta / minL);
+        per = q > 4e18 ? (LLONG_MAX / 4) : (long long)q + 2;
+    }
+    g->ceiling = per > LLONG_MAX / n ? LLONG_MAX : n * per;
+    const size_t esz = mode == DS_MODE_FIXED32 ? sizeof(uint2) : sizeof(EdgeF64);
+    if ((rc = ensure_edges(&g->Ledges, &g->Lcap, esz * (size_t)g->nL))) return rc;
+    if ((rc = ensure_edges(&g->Hedges, &g->Hcap, esz * (size_t)g->nH))) return rc;
+    if (mode == DS_MODE_FIXED32)
+        k_split_scatter<uint2><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, delta, g->frac,
+                                                            g->Lptr, g->Hptr, (uint2*)g->Ledges,
+                                                            (uint2*)g->Hedges);
+    else
+        k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, delta, 0,
+                                                              g->Lptr, g->Hptr, (EdgeF64*)g->Ledges,
+                                                              (EdgeF64*)g->Hedges);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(g->ev1, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+    g->prep_ms = ms;
+    g->delta = delta;
+    g->prepared = true;
+    return DS_OK;
+}
+
+extern "C" int ds_graph_prepare(ds_graph* g, double delta, uint32_t flags, ds_prep_info* info) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    DeviceGuard guard(g->device);
+    int rc = prepare(g, delta, flags);
+    if (rc) return rc;
+    if (info) {
+        info->nnz_light = g->nL;
+        info->nnz_heavy = g->nH;
+        info->min_light_weight = g->minL;
+        info->phase_ceiling = g->ceiling;
+        info->dist_mode = g->mode;
+        info->frac_bits = g->frac;
+        info->prepare_ms = g->prep_ms;
+    }
+    return DS_OK;
+}
+
+template <class M>
+static int launch_solve(ds_graph* g, long long source, int* dev_status) {
+    KParams<M> p{};
+    p.n = g->n;
+    p.source = source;
+    p.delta = g->delta;
+    p.frac = g->frac;
+    p.ceiling = g->ceiling;
+    double tmo = 120.0;
+    if (const char* s = getenv("DS_TIMEOUT_S")) tmo = atof(s);
+    p.timeout_ns = (unsigned long long)(tmo * 1e9);
+    p.indptr = g->indptr;
+    p.Lptr = g->Lptr;
+    p.Ledges = (const typename M::Edge*)g->Ledges;
+    p.Hptr = g->Hptr;
+    p.Hedges = (const typename M::Edge*)g->Hedges;
+    p.dist = (typename M::D*)g->dist;
+    p.fstamp = g->fstamp;
+    p.sstamp = g->sstamp;
+    p.F0 = g->F0;
+    p.F1 = g->F1;
+    p.S = g->S;
+    p.Rpre = g->Rpre;
+    p.Rbase = g->Rbase;
+    p.Rd = (typename M::D*)g->Rd;
+    p.tile_start = g->tile_start;
+    p.tflag = g->tflag;
+    p.tagg = g->tagg;
+    p.tinc = g->tinc;
+    p.ctl = g->ctl;
+    p.out = g->out;
+    p.pser0 = g->pser;
+    p.bser0 = g->bser;
+    p.sser0 = g->sser;
+    const unsigned grid = (unsigned)(std::is_same<M, ModeFixed>::value ? g->grid_fixed : g->grid_f64);
+    CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
+    void* args[] = {(void*)&p};
+    CK(cudaEventRecord(g->ev0, g->stream));
+    CK(cudaLaunchCooperativeKernel((const void*)sssp_persistent_kernel<M>, dim3(grid), dim3(kThreads),
+                                   args, 0, g->stream));
+    CK(cudaEventRecord(g->ev1, g->stream));
+    CK(cudaMemcpyAsync(g->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    const Ctl& c = *g->h_ctl;
+    // advance serials past everything this launch used
+    g->pser += (unsigned)(c.phases + 4);
+    g->bser += (unsigned)(c.visited + c.phases + 4);
+    g->sser += c.steps + 4;
+    if (g->pser > 0x7FFFFFFFu || g->bser > 0x7FFFFFFFu) {
+        CK(cudaMemsetAsync(g->fstamp, 0, sizeof(unsigned) * g->n, g->stream));
+        CK(cudaMemsetAsync(g->sstamp, 0, sizeof(unsigned) * g->n, g->stream));
+        g->pser = g->bser = 1;
+    }
+    if (c.abort) return set_err(DS_ETIMEOUT, "solver watchdog expired (DS_TIMEOUT_S=%g)", tmo);
+    *dev_status = c.status;
+    return DS_OK;
+}
+
+extern "C" int ds_sssp(ds_graph* g, int64_t source, double delta, uint32_t flags, ds_stats* stats) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    if (!(source >= 0 && source < g->n))
+        return set_err(DS_EINVAL, "source %lld out of range for %lld vertices", (long long)source,
+                       (long long)g->n);
+    if (!(delta > 0) || !std::isfinite(delta))
+        return set_err(DS_EINVAL, "delta must be a positive finite number, got %g", delta);
+    DeviceGuard guard(g->device);
+    int fallbacks = 0;
+    for (;;) {
+        int rc = prepare(g, delta, flags);
+        if (rc) return rc;
+        int st = 0;
+        rc = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, source, &st)
+                                        : launch_solve<ModeF64>(g, source, &st);
+        if (rc) return rc;
+        if (st == kDevOverflow) {
+            // a fixed-point distance would exceed 32 bits: redo in binary64
+            g->overflow_delta = delta;
+            ++fallbacks;
+            if (fallbacks > 1) return set_err(DS_ECUDA, "unexpected overflow in f64 mode");
+            continue;
+        }
+        if (st == DS_ENOCONVERGE)
+            return set_err(DS_ENOCONVERGE,
+                           "light phase count exceeded ceiling %lld; relaxation is not converging",
+                           g->ceiling);
+        if (st != 0) return set_err(DS_ECUDA, "device solver status %d", st);
+        break;
+    }
+    const Ctl& c = *g->h_ctl;
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+    double maxd;
+    if (g->mode == DS_MODE_FIXED32)
+        maxd = ldexp((double)(unsigned)c.max_d, -g->frac);
+    else
+        memcpy(&maxd, &c.max_d, 8);
+    g->have_result = true;
+    g->reached = (long long)c.reached;
+    if (stats) {
+        stats->inner_phases = (int64_t)c.phases;
+        stats->buckets_visited = (int64_t)c.visited;
+        // non-skip outer loop stops at the first i with max(t) < i*delta
+        // (sssp.py:280), i.e. bucket_index_of(max t) + 1
+        const long long nonskip = bucket_index_of(maxd, delta) + 1;
+        stats->outer_iterations = (flags & DS_FLAG_SKIP_EMPTY) ? (int64_t)c.visited : nonskip;
+        stats->reached = (int64_t)c.reached;
+        stats->edges_reached = (int64_t)c.edges_reached;
+        stats->edges_scanned = (int64_t)c.edges_scanned;
+        stats->grid_barriers = (int64_t)c.barriers;
+        stats->max_distance = maxd;
+        stats->kernel_ms = ms;
+        stats->dist_mode = g->mode;
+        stats->fallbacks = fallbacks;
+    }
+    return DS_OK;
+}
+
+extern "C" int ds_result_dense(ds_graph* g, double* out) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    if (!g->have_result) return set_err(DS_EINVAL, "no solve result on this handle");
+    DeviceGuard guard(g->device);
+    CK(cudaMemcpyAsync(out, g->out, sizeof(double) * g->n, cudaMemcpyDefault, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    return DS_OK;
+}
+
+extern "C" int ds_result_sparse(ds_graph* g, int64_t* idx, double* val) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    if (!g->have_result) return set_err(DS_EINVAL, "no solve result on this handle");
+    DeviceGuard guard(g->device);
+    const long long n = g->n;
+    const long long nblk = (n + kCompTile - 1) / kCompTile;
+    if (!g->cidx) CK(cudaMalloc(&g->cidx, sizeof(long long) * n));
+    if (!g->ccount) CK(cudaMalloc(&g->ccount, sizeof(unsigned long long) * (2 * nblk + 2)));
+    unsigned long long* counts = g->ccount;
+    unsigned long long* offs = g->ccount + nblk + 1;
+    k_compact_count<<<(unsigned)nblk, kThreads, 0, g->stream>>>(g->out, n, counts);
+    CK(cudaGetLastError());
+    size_t bytes = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, offs, nblk, g->stream));
+    int rc = ensure_cub(g, bytes);
+    if (rc) return rc;
+    CK(cub::DeviceScan::ExclusiveSum(g->cub_tmp, bytes, counts, offs, nblk, g->stream));
+    // values land in Rbase-sized scratch reinterpreted as double (n entries)
+    double* cval = reinterpret_cast<double*>(g->Rbase);
+    k_compact_write<<<(unsigned)nblk, kThreads, 0, g->stream>>>(g->out, n, offs, g->cidx, cval);
+    CK(cudaGetLastError());
+    const long long r = g->reached;
+    if (r > 0) {
+        CK(cudaMemcpyAsync(idx, g->cidx, sizeof(long long) * r, cudaMemcpyDefault, g->stream));
+        CK(cudaMemcpyAsync(val, cval, sizeof(double) * r, cudaMemcpyDefault, g->stream));
+    }
+    CK(cudaStreamSynchronize(g->stream));
+    return DS_OK;
+}
+
+template <class Edge>
+__global__ void k_export_edges(const Edge* e, long long m, int frac, long long* col, double* val);
+
+template <>
+__global__ void k_export_edges<uint2>(const uint2* e, long long m, int frac, long long* col, double* val) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+         i += (long long)gridDim.x * blockDim.x) {
+        col[i] = e[i].x;
+        val[i] = ldexp((double)e[i].y, -frac);
+    }
+}
+template <>
+__global__ void k_export_edges<EdgeF64>(const EdgeF64* e, long long m, int, long long* col, double* val) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+         i += (long long)gridDim.x * blockDim.x) {
+        col[i] = e[i].col;
+        val[i] = e[i].w;
+    }
+}
+
+extern "C" int ds_export_split(ds_graph* g, int which, int64_t* indptr, int64_t* col, double* val) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    if (!g->prepared) return set_err(DS_EINVAL, "graph not prepared");
+    DeviceGuard guard(g->device);
+    const long long m = which ? g->nH : g->nL;
+    const long long* ptr = which ? g->Hptr : g->Lptr;
+    CK(cudaMemcpyAsync(indptr, ptr, sizeof(long long) * (g->n + 1), cudaMemcpyDefault, g->stream));
+    if (m > 0) {
+        long long* dcol = nullptr;
+        double* dval = nullptr;
+        CK(cudaMalloc(&dcol, sizeof(long long) * m));
+        CK(cudaMalloc(&dval, sizeof(double) * m));
+        if (g->mode == DS_MODE_FIXED32)
+            k_export_edges<uint2><<<elementwise_grid(g), 256, 0, g->stream>>>(
+                (const uint2*)(which ? g->Hedges : g->Ledges), m, g->frac, dcol, dval);
+        else
+            k_export_edges<EdgeF64><<<elementwise_grid(g), 256, 0, g->stream>>>(
+                (const EdgeF64*)(which ? g->Hedges : g->Ledges), m, 0, dcol, dval);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(col, dcol, sizeof(long long) * m, cudaMemcpyDefault, g->stream));
+        CK(cudaMemcpyAsync(val, dval, sizeof(double) * m, cudaMemcpyDefault, g->stream));
+        CK(cudaStreamSynchronize(g->stream));
+        cudaFree(dcol);
+        cudaFree(dval);
+    }
+    CK(cudaStreamSynchronize(g->stream));
+    return DS_OK;
+}
+
+__global__ void k_download_w(const double* w, float* out, long long m, int* bad) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+         i += (long long)gridDim.x * blockDim.x) {
+        const float f = (float)w[i];
+        if ((double)f != w[i]) atomicOr(bad, 1);
+        out[i] = f;
+    }
+}
+
+extern "C" int ds_graph_download(ds_graph* g, int64_t* indptr, int32_t* col, float* val) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    DeviceGuard guard(g->device);
+    CK(cudaMemcpyAsync(indptr, g->indptr, sizeof(long long) * (g->n + 1), cudaMemcpyDefault, g->stream));
+    if (g->nnz > 0) {
+        CK(cudaMemcpyAsync(col, g->col, sizeof(int) * g->nnz, cudaMemcpyDefault, g->stream));
+        float* tmp = nullptr;
+        CK(cudaMalloc(&tmp, sizeof(float) * g->nnz));
+        int* bad = reinterpret_cast<int*>(g->pstat);
+        CK(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
+        k_download_w<<<elementwise_grid(g), 256, 0, g->stream>>>(g->w, tmp, g->nnz, bad);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(val, tmp, sizeof(float) * g->nnz, cudaMemcpyDefault, g->stream));
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+        CK(cudaStreamSynchronize(g->stream));
+        cudaFree(tmp);
+        if (h) return set_err(DS_EINVAL, "weights are not float32-exact");
+    }
+    CK(cudaStreamSynchronize(g->stream));
+    return DS_OK;
+}
+
+// ds_gen_rmat lives in gen.cu; it builds the CSR on the device and adopts it.
+int ds_internal_adopt(ds_graph** out, int device, void* stream, long long n, long long nnz,
+                      long long* indptr, int* col, double* w) {
+    ds_graph* g = new ds_graph();
+    g->device = device;
+    g->stream = (cudaStream_t)stream;
+    g->n = n;
+    g->nnz = nnz;
+    cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, device);
+    g->indptr = indptr;
+    g->col = col;
+    g->w = w;
+    int rc = alloc_scratch(g);
+    if (rc) {
+        free_all(g);
+        delete g;
+        return rc;
+    }
+    *out = g;
+    return DS_OK;
+}
+
+int ds_internal_set_err(int code, const char* msg) { return set_err(code, "%s", msg); }

@@ -1,0 +1,325 @@
+"""Drop-in `delta_stepping` on the B200 (the reference's sssp.py:239-313 API).
+
+The host side keeps the reference's Python signature, argument validation,
+exception types/messages and result shape; everything between "CSR in" and
+"distances out" runs in the sm_100a library behind the C-ABI
+(include/dsssp.h) -- device CSR with a per-delta light/heavy split, then one
+persistent cooperative kernel per source.  There is no CPU fallback: without
+libdsssp.so or a CUDA device the call raises.
+
+Reference interface mirrored (file:line under /root/reference/pkg/src/deltasparse):
+  delta_stepping      sssp.py:239-313   (validation :255-260, ceiling :297-301)
+  SsspResult          sssp.py:82-87
+  split_edges         sssp.py:106-150   (device split, exported back to host)
+  BackendChoice       fused.py:41-55    (validated, then ignored: one GPU path)
+  bucket_bounds       fused.py:58-61
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import threading
+import time
+from collections import OrderedDict
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .containers import SparseMatrix, SparseVector
+
+__all__ = [
+    "BackendChoice",
+    "SsspResult",
+    "DeviceGraph",
+    "bucket_bounds",
+    "delta_stepping",
+    "split_edges",
+    "clear_device_cache",
+]
+
+
+@dataclass(frozen=True)
+class BackendChoice:
+    """Accepted for call-site compatibility with the reference (fused.py:41-55).
+
+    The B200 build has exactly one implementation; `kind`, `workers` and
+    `chunks_per_worker` are validated like the reference and otherwise
+    ignored (no multi-backend dispatch).
+    """
+
+    kind: str = "unfused"
+    workers: int = 1
+    chunks_per_worker: int = 1
+
+    def __post_init__(self) -> None:
+        if self.kind not in ("unfused", "fused"):
+            raise ValueError(f"backend kind must be 'unfused' or 'fused', got {self.kind!r}")
+        if self.workers < 1:
+            raise ValueError(f"workers must be >= 1, got {self.workers}")
+        if self.chunks_per_worker < 1:
+            raise ValueError(f"chunks_per_worker must be >= 1, got {self.chunks_per_worker}")
+
+
+@dataclass(frozen=True)
+class SsspResult:
+    """Same fields as the reference (sssp.py:82-87); `device_stats` carries
+    the solver's counters (n_r, m_r, kernel time, ...) and is excluded from
+    comparisons."""
+
+    distances: SparseVector
+    outer_iterations: int
+    inner_phases: int
+    elapsed: float
+    device_stats: dict | None = field(default=None, compare=False, repr=False)
+
+
+def bucket_bounds(index: int, delta: float) -> tuple[float, float]:
+    """Half-open window of bucket `index` (fused.py:58-61)."""
+    return index * delta, (index + 1) * delta
+
+
+def _ptr(a) -> int:
+    if a is None:
+        return 0
+    if hasattr(a, "data_ptr"):  # torch tensor (host pinned or device)
+        return int(a.data_ptr())
+    return int(a.ctypes.data)
+
+
+def _col_dtype(dt) -> int:
+    if dt == np.int32:
+        return _lib.DS_IDX_I32
+    if dt == np.int64:
+        return _lib.DS_IDX_I64
+    raise ValueError(f"unsupported column dtype {dt}")
+
+
+def _val_dtype(dt) -> int:
+    if dt == np.float32:
+        return _lib.DS_W_F32
+    if dt == np.float64:
+        return _lib.DS_W_F64
+    if dt == np.int32:
+        return _lib.DS_W_I32
+    raise ValueError(f"unsupported weight dtype {dt}")
+
+
+class DeviceGraph:
+    """A graph resident in HBM: one `ds_graph` handle of the C-ABI library."""
+
+    def __init__(self, handle: int, n: int, nnz: int, device: int):
+        self._h = ctypes.c_void_p(handle)
+        self.n = int(n)
+        self.nnz = int(nnz)
+        self.device = int(device)
+        self.last_stats: _lib.Stats | None = None
+        self.prep: _lib.PrepInfo | None = None
+
+    # -- construction ---------------------------------------------------
+    @classmethod
+    def from_csr(cls, n, indptr, col, val, device: int = 0, stream: int | None = None) -> "DeviceGraph":
+        """Upload a CSR.  numpy arrays (host) or torch tensors (pinned host or
+        device) are accepted; dtypes int32/int64 columns, float32/float64/int32
+        weights."""
+        L = _lib.lib()
+
+        def dt(a):
+            return np.dtype(str(a.dtype).replace("torch.", "")) if hasattr(a, "data_ptr") else a.dtype
+
+        if not hasattr(indptr, "data_ptr"):
+            indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+        if not hasattr(col, "data_ptr"):
+            col = np.ascontiguousarray(col)
+            if col.dtype not in (np.int32, np.int64):
+                col = col.astype(np.int64)
+        if not hasattr(val, "data_ptr"):
+            val = np.ascontiguousarray(val)
+            if val.dtype not in (np.float32, np.float64, np.int32):
+                val = val.astype(np.float64)
+        nnz = int(col.shape[0])
+        h = ctypes.c_void_p()
+        _lib.check(L.ds_graph_create(int(n), nnz, _ptr(indptr), _ptr(col), _col_dtype(dt(col)),
+                                     _ptr(val), _val_dtype(dt(val)), int(device), stream or 0,
+                                     ctypes.byref(h)))
+        return cls(h.value, n, nnz, device)
+
+    @classmethod
+    def from_matrix(cls, matrix, device: int = 0, stream: int | None = None) -> "DeviceGraph":
+        return cls.from_csr(matrix.n, matrix.indptr, matrix.col, matrix.val, device, stream)
+
+    @classmethod
+    def rmat(cls, scale: int, edge_factor: int = 16, seed: int = 1, weight_seed: int = 2,
+             device: int = 0, stream: int | None = None) -> "DeviceGraph":
+        """R-MAT generated on the device; identical to graphs.rmat()."""
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        _lib.check(L.ds_gen_rmat(int(scale), int(edge_factor), int(seed), int(weight_seed),
+                                 int(device), stream or 0, ctypes.byref(h)))
+        n = ctypes.c_int64()
+        nnz = ctypes.c_int64()
+        _lib.check(L.ds_graph_size(h, ctypes.byref(n), ctypes.byref(nnz)))
+        return cls(h.value, n.value, nnz.value, device)
+
+    # -- operations -----------------------------------------------------
+    def _handle(self):
+        if not self._h.value:
+            raise ValueError("device graph is closed")
+        return self._h
+
+    def set_stream(self, stream: int | None) -> None:
+        _lib.check(_lib.lib().ds_graph_set_stream(self._handle(), stream or 0))
+
+    def prepare(self, delta: float, force_f64: bool = False) -> _lib.PrepInfo:
+        info = _lib.PrepInfo()
+        flags = _lib.DS_FLAG_FORCE_F64 if force_f64 else 0
+        _lib.check(_lib.lib().ds_graph_prepare(self._handle(), float(delta), flags,
+                                               ctypes.byref(info)))
+        self.prep = info
+        return info
+
+    def solve(self, source: int, delta: float, skip_empty_buckets: bool = False,
+              force_f64: bool = False) -> _lib.Stats:
+        st = _lib.Stats()
+        flags = (_lib.DS_FLAG_SKIP_EMPTY if skip_empty_buckets else 0) | (
+            _lib.DS_FLAG_FORCE_F64 if force_f64 else 0)
+        _lib.check(_lib.lib().ds_sssp(self._handle(), int(source), float(delta), flags,
+                                      ctypes.byref(st)))
+        self.last_stats = st
+        return st
+
+    def result_dense(self, out=None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.n, dtype=np.float64)
+        _lib.check(_lib.lib().ds_result_dense(self._handle(), _ptr(out)))
+        return out
+
+    def result_sparse(self, out=None):
+        """(indices int64, values float64) of reached vertices; `out` may be a
+        pair of preallocated (pinned) buffers with >= reached entries."""
+        r = int(self.last_stats.reached) if self.last_stats is not None else self.n
+        if out is None:
+            idx = np.empty(r, dtype=np.int64)
+            val = np.empty(r, dtype=np.float64)
+        else:
+            idx, val = out[0][:r], out[1][:r]
+        _lib.check(_lib.lib().ds_result_sparse(self._handle(), _ptr(idx), _ptr(val)))
+        return idx, val
+
+    def export_split(self, which: int):
+        """Light (0) / heavy (1) CSR of the current prepare as host arrays."""
+        if self.prep is None:
+            raise ValueError("export_split needs a prepare() first")
+        m = int(self.prep.nnz_heavy if which else self.prep.nnz_light)
+        indptr = np.empty(self.n + 1, dtype=np.int64)
+        col = np.empty(max(m, 1), dtype=np.int64)
+        val = np.empty(max(m, 1), dtype=np.float64)
+        _lib.check(_lib.lib().ds_export_split(self._handle(), int(which), _ptr(indptr), _ptr(col),
+                                              _ptr(val)))
+        return indptr, col[:m], val[:m]
+
+    def download(self):
+        """Original CSR (int64 indptr, int32 col, float32 val) to host."""
+        indptr = np.empty(self.n + 1, dtype=np.int64)
+        col = np.empty(max(self.nnz, 1), dtype=np.int32)
+        val = np.empty(max(self.nnz, 1), dtype=np.float32)
+        _lib.check(_lib.lib().ds_graph_download(self._handle(), _ptr(indptr), _ptr(col), _ptr(val)))
+        return indptr, col[: self.nnz], val[: self.nnz]
+
+    def close(self) -> None:
+        if self._h.value:
+            _lib.lib().ds_graph_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ cache
+# The reference caches derived data (transposed views) on the matrix object
+# (core.py:128, 289-301).  Its SparseMatrix has __slots__ without __weakref__,
+# so the device copy is cached here keyed on object identity, holding a
+# strong reference to the matrix so the id cannot be recycled while cached.
+
+_CACHE: "OrderedDict[int, tuple[object, DeviceGraph]]" = OrderedDict()
+_CACHE_SIZE = 2
+_CACHE_LOCK = threading.Lock()
+
+
+def clear_device_cache() -> None:
+    with _CACHE_LOCK:
+        for _, g in _CACHE.values():
+            g.close()
+        _CACHE.clear()
+
+
+def _device_graph(matrix, device: int = 0) -> DeviceGraph:
+    key = id(matrix)
+    with _CACHE_LOCK:
+        hit = _CACHE.get(key)
+        if hit is not None and hit[0] is matrix:
+            _CACHE.move_to_end(key)
+            return hit[1]
+        g = DeviceGraph.from_matrix(matrix, device)
+        _CACHE[key] = (matrix, g)
+        while len(_CACHE) > _CACHE_SIZE:
+            _, (_, old) = _CACHE.popitem(last=False)
+            old.close()
+        return g
+
+
+# ------------------------------------------------------------------ API
+
+def delta_stepping(
+    matrix,
+    source: int,
+    delta: float,
+    *,
+    backend: BackendChoice | None = None,
+    skip_empty_buckets: bool = False,
+) -> SsspResult:
+    """Single-source shortest paths by delta-stepping on the GPU.
+
+    Same contract as the reference (sssp.py:239-313): `matrix` is any CSR
+    object with `.n/.indptr/.col/.val` (ours or `deltasparse.SparseMatrix`);
+    returns the reached vertices' float64 distances bit-identical to the
+    reference, with identical `outer_iterations` / `inner_phases`.
+    `elapsed` covers the device split (cached per delta) and the solve, like
+    the reference's (sssp.py:263, 312).
+    """
+    if backend is None:
+        backend = BackendChoice()
+    if not 0 <= source < matrix.n:
+        raise ValueError(f"source {source} out of range for {matrix.n} vertices")
+    if not (delta > 0) or not math.isfinite(delta):
+        raise ValueError(f"delta must be a positive finite number, got {delta}")
+    start = time.perf_counter()
+    g = _device_graph(matrix)
+    st = g.solve(int(source), float(delta), skip_empty_buckets=skip_empty_buckets)
+    idx, val = g.result_sparse()
+    elapsed = time.perf_counter() - start
+    return SsspResult(
+        distances=SparseVector(matrix.n, idx, val),
+        outer_iterations=int(st.outer_iterations),
+        inner_phases=int(st.inner_phases),
+        elapsed=elapsed,
+        device_stats=st.as_dict(),
+    )
+
+
+def split_edges(matrix, delta: float, workers: int = 1, chunks_per_worker: int = 1):
+    """Light/heavy partition (sssp.py:106-150) computed by the device split
+    kernels and returned as host `SparseMatrix` objects."""
+    if not (delta > 0) or not math.isfinite(delta):
+        raise ValueError(f"delta must be a positive finite number, got {delta}")
+    g = _device_graph(matrix)
+    g.prepare(float(delta))
+    out = []
+    for which in (0, 1):
+        indptr, col, val = g.export_split(which)
+        out.append(SparseMatrix(matrix.n, indptr, col, val))
+    return out[0], out[1]

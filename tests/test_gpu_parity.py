@@ -1,0 +1,247 @@
+"""GPU parity: the sm_100a path (through the C-ABI library) against golden
+vectors recorded from the reference and against the CPU oracle.
+
+Bit-exact for distances (float64 bit patterns) and exact for the
+reference's counters (outer_iterations, inner_phases, skip-mode outer).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import criterion1_graphs, csr_hash, graph_from_json, unit_graphs, vec_hash
+from paper_1911_06895_b200 import (
+    BackendChoice,
+    DeviceGraph,
+    SparseMatrix,
+    clear_device_cache,
+    delta_stepping,
+    graphs,
+    matrix_build,
+    split_edges,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def check_run(matrix, source, run):
+    d = float.fromhex(run["delta"])
+    r = delta_stepping(matrix, source, d)
+    assert vec_hash(r.distances.indices, r.distances.values) == run["hash"], (source, d)
+    assert r.outer_iterations == run["outer"]
+    assert r.inner_phases == run["phases"]
+    rs = delta_stepping(matrix, source, d, skip_empty_buckets=True,
+                        backend=BackendChoice("fused", workers=4))
+    assert rs.distances == r.distances
+    assert rs.outer_iterations == run["outer_skip"]
+    assert rs.inner_phases == run["phases_skip"]
+    if "values" in run:
+        assert r.distances.indices.tolist() == run["indices"]
+        assert [float(x).hex() for x in r.distances.values] == run["values"]
+    return r
+
+
+def test_hand_cases(golden):
+    for name, case in golden["hand"].items():
+        n, indptr, col, val = graph_from_json(case["graph"])
+        a = SparseMatrix(n, indptr, col, val)
+        for run in case["runs"]:
+            check_run(a, case["source"], run)
+
+
+def test_reference_hand_values():
+    # test_sssp.py:161-181, 211-219: exact float bits of the traces
+    a = matrix_build(3, [(0, 1, 0.4), (1, 2, 0.4), (0, 2, 0.9)])
+    assert delta_stepping(a, 0, 1.0).distances.to_dict() == {0: 0.0, 1: 0.4, 2: 0.4 + 0.4}
+    b = matrix_build(4, [(0, 1, 0.4), (0, 3, 5.0), (1, 3, 4.2)])
+    assert delta_stepping(b, 0, 1.0).distances.get(3) == 0.4 + 4.2
+    c = matrix_build(4, [(0, 1, 1.0), (1, 2, 1.0), (2, 3, 1.0)])
+    r = delta_stepping(c, 0, 1.0)
+    assert r.distances.to_dict() == {0: 0.0, 1: 1.0, 2: 2.0, 3: 3.0}
+    assert (r.outer_iterations, r.inner_phases) == (4, 4)
+    one = matrix_build(1, [])
+    r = delta_stepping(one, 0, 1.0)
+    assert r.distances.to_dict() == {0: 0.0} and r.outer_iterations == 1
+
+
+def test_trusting_constructor_weights(golden):
+    # zero / negative / inf / nan weights vanish in the split (sssp.py:96-97)
+    for case in golden["trusting"]:
+        n, indptr, col, val = graph_from_json(case["graph"])
+        a = SparseMatrix(n, indptr, col, val)
+        for run in case["runs"]:
+            check_run(a, case["source"], run)
+
+
+def test_criterion1_corpus(golden, corpus_dist):
+    offs = corpus_dist["offsets"]
+    for (a, s, kind), rec in zip(criterion1_graphs(), golden["criterion1"]):
+        assert csr_hash(a.indptr, a.col, a.val) == rec["graph_hash"]
+        for run in rec["runs"]:
+            check_run(a, s, run)
+        if rec["case"] < 100:
+            c = rec["case"]
+            r = delta_stepping(a, s, 1.0)
+            assert np.array_equal(r.distances.indices, corpus_dist["indices"][offs[c]:offs[c + 1]])
+            assert bits_equal(r.distances.values, corpus_dist["values"][offs[c]:offs[c + 1]])
+    clear_device_cache()
+
+
+def test_odd_delta_rounding_corpus(golden):
+    for rec in golden["odd_delta"]:
+        n, indptr, col, val = graph_from_json(rec["graph"])
+        a = SparseMatrix(n, indptr, col, val)
+        for run in rec["runs"]:
+            check_run(a, rec["source"], run)
+
+
+def test_unit_corpus(golden):
+    for a, rec in zip(unit_graphs(), golden["unit"]):
+        r = check_run(a, 0, rec["runs"][0])
+        assert r.distances.nnz == a.n
+        assert r.inner_phases == r.outer_iterations
+
+
+def test_baseline_shaped_small(golden):
+    bs = golden["baseline_shaped"]
+    er = graphs.erdos_renyi(1024, seed=0)
+    check_run(er, 0, bs["er1024"]["runs"][0])
+    for scale in (10, 12):
+        g = graphs.rmat(scale, seed=1, weight_seed=2)
+        for run in bs[f"rmat{scale}"]["runs"]:
+            check_run(g, run["source"], run)
+    for side in (32, 64):
+        g = graphs.grid2d(side, seed=3)
+        check_run(g, 0, bs[f"grid{side}"]["runs"][0])
+
+
+def test_split_edges_parity(golden):
+    for rec in golden["split"]:
+        n, indptr, col, val = graph_from_json(rec["graph"])
+        a = SparseMatrix(n, indptr, col, val)
+        light, heavy = split_edges(a, float.fromhex(rec["delta"]))
+        assert csr_hash(light.indptr, light.col, light.val) == rec["light"]
+        assert csr_hash(heavy.indptr, heavy.col, heavy.val) == rec["heavy"]
+
+
+def test_argument_errors_match_reference():
+    a = matrix_build(3, [(0, 1, 1.0)])
+    with pytest.raises(ValueError, match="out of range"):
+        delta_stepping(a, 3, 1.0)
+    with pytest.raises(ValueError):
+        delta_stepping(a, -1, 1.0)
+    for bad in (0.0, -2.0, math.inf, math.nan):
+        with pytest.raises(ValueError, match="delta must be a positive finite number"):
+            delta_stepping(a, 0, bad)
+    with pytest.raises(ValueError):
+        split_edges(a, 0.0)
+
+
+def test_invalid_csr_rejected_by_device_library():
+    with pytest.raises(ValueError, match="column index out of range"):
+        DeviceGraph.from_csr(3, np.array([0, 1, 1, 1]), np.array([7]), np.array([1.0]))
+    with pytest.raises(ValueError, match="indptr"):
+        DeviceGraph.from_csr(3, np.array([0, 2, 1, 1]), np.array([1]), np.array([1.0]))
+
+
+def test_fixed_point_overflow_falls_back_to_f64():
+    # integer weights fit 32 bits but path sums do not -> exact f64 rerun
+    w = float(2**31)
+    a = matrix_build(4, [(0, 1, w), (1, 2, w), (2, 3, w)])
+    r = delta_stepping(a, 0, 1e9)
+    assert r.distances.to_dict() == {0: 0.0, 1: w, 2: 2 * w, 3: 3 * w}
+    assert r.device_stats["fallbacks"] == 1
+    want, outer, phases = oracle.delta_stepping(4, a.indptr, a.col, a.val, 0, 1e9)
+    assert bits_equal(r.distances.to_dense(), want)
+    assert (r.outer_iterations, r.inner_phases) == (outer, phases)
+
+
+def _dense_check(g: DeviceGraph, a, source, delta, threads, force_f64=False):
+    st = g.solve(source, delta, force_f64=force_f64)
+    got = g.result_dense()
+    want, outer, phases = oracle.delta_stepping(a.n, a.indptr, a.col, a.val, source, delta,
+                                                threads=threads)
+    assert bits_equal(got, want), (source, delta)
+    assert st.inner_phases == phases
+    assert st.outer_iterations == outer
+    return st
+
+
+def test_rmat18_sources_vs_oracle():
+    a = graphs.rmat(18, seed=1, weight_seed=2)
+    g = DeviceGraph.from_matrix(a)
+    threads = max(1, oracle.max_threads())
+    for s in graphs.pick_sources(a.indptr, 16, seed=7):
+        st = _dense_check(g, a, s, 0.1, threads)
+        assert st.dist_mode == 0  # exact fixed-point path
+    s0 = graphs.pick_sources(a.indptr, 1, seed=11)[0]
+    for d in (0.05, 0.25):
+        _dense_check(g, a, s0, d, threads)
+    # binary64 path gives the same bits
+    st = _dense_check(g, a, s0, 0.1, threads, force_f64=True)
+    assert st.dist_mode == 1
+    g.close()
+
+
+def test_er1024_config():
+    a = graphs.erdos_renyi(1024, seed=0)
+    g = DeviceGraph.from_matrix(a)
+    for s in range(0, 1024, 97):
+        _dense_check(g, a, s, 3.0, 1)
+    g.close()
+
+
+def test_grid_256_vs_oracle():
+    a = graphs.grid2d(256, seed=3)
+    g = DeviceGraph.from_matrix(a)
+    _dense_check(g, a, 0, 25.0, max(1, oracle.max_threads()))
+    g.close()
+
+
+def test_device_rmat_generator_matches_host():
+    for scale in (8, 12):
+        host = graphs.rmat(scale, seed=1, weight_seed=2)
+        dev = DeviceGraph.rmat(scale, 16, 1, 2)
+        indptr, col, val = dev.download()
+        assert np.array_equal(indptr, host.indptr)
+        assert np.array_equal(col, host.col)
+        assert np.array_equal(val, host.val)
+        dev.close()
+
+
+def test_grid_4096_vs_dijkstra():
+    a = graphs.grid2d(4096, seed=3)
+    g = DeviceGraph.from_matrix(a)
+    st = g.solve(0, 25.0)
+    got = g.result_dense()
+    want = oracle.dijkstra(a.n, a.indptr, a.col, a.val, 0)
+    assert bits_equal(got, want)
+    assert st.reached == a.n
+    # skip-mode outer counts non-empty buckets; non-skip is max(d)//delta + 1
+    assert st.outer_iterations == math.floor(want.max() / 25.0) + 1
+    g.close()
+
+
+def test_rmat20_fixed_vs_f64_and_dijkstra():
+    g = DeviceGraph.rmat(20, 16, 1, 2)
+    indptr, col, val = g.download()
+    s = graphs.pick_sources(indptr, 1, seed=7)[0]
+    st = g.solve(s, 0.1)
+    fixed = g.result_dense()
+    st64 = g.solve(s, 0.1, force_f64=True)
+    f64 = g.result_dense()
+    assert bits_equal(fixed, f64)
+    assert (st.inner_phases, st.outer_iterations) == (st64.inner_phases, st64.outer_iterations)
+    want = oracle.dijkstra(g.n, indptr, col, val, s)
+    assert bits_equal(fixed, want)
+    g.close()
