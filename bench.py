@@ -1,0 +1,453 @@
+"""Benchmark: SSSP GTEPS + achieved HBM GB/s on R-MAT (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[3], the single-GPU headline): R-MAT scale 24,
+edge factor 16, a,b,c,d = .57,.19,.19,.05, symmetrised + deduplicated,
+fp32-lattice weights, delta = 0.1, seeded random sources with nonzero degree.
+One step = one batch of `--batch` sources solved on the resident graph.
+
+* value  : GTEPS = sum(m_r) / device time of the K timed steps (graph and its
+           light/heavy split already in HBM; CUDA events on the solver's
+           stream; max over ranks).  m_r = out-degree sum of reached vertices.
+* e2e    : the same metric through the public API with HOST buffers: every
+           step uploads the CSR from pinned host memory, splits it, solves the
+           batch and copies every distance vector back (SparseVector shape).
+* roofline: algorithmic bytes per solve B_alg = 8 m_r + 16 n_r + 8 n
+            / mean kernel time vs MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline: the reference algorithm restated in C (oracle/, OpenMP) on
+           the box's host cores, one source of the same graph.
+
+Multi-GPU (torchrun): sources are independent, so each rank solves its own
+batch on a replica of the graph (weak scaling, no data-path collective).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "SSSP GTEPS (edges relaxed/s) on RMAT graphs"
+UNIT = "GTEPS"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--scale", type=int, default=24)
+    ap.add_argument("--edge-factor", type=int, default=16)
+    ap.add_argument("--delta", type=float, default=0.1)
+    ap.add_argument("--batch", type=int, default=8, help="sources per step (per rank)")
+    ap.add_argument("--sources", type=int, default=64, help="source pool (BASELINE: 64)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also time delta in {0.05, 0.25}")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def b_alg(m_r: int, n_r: int, n: int) -> int:
+    """Algorithmic bytes per solve: one (col, w) pair per
+    edge of a reached vertex, 2 int64 row offsets per reached vertex, one
+    8-byte distance write per vertex."""
+    return 8 * m_r + 16 * n_r + 8 * n
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ CPU arm
+
+def run_cpu_oracle(indptr, col, val, sources, delta, threads):
+    """Reference algorithm (oracle/, C restatement of sssp.py:239-313 with the
+    reference's dense pull, OpenMP over rows like parallel_execute) on host
+    cores.  Returns (seconds, sum m_r) for the given sources."""
+    import numpy as np
+
+    import oracle
+
+    deg = np.diff(indptr)
+    total_t, total_m = 0.0, 0
+    for s in sources:
+        t0 = time.perf_counter()
+        dist, _, _ = oracle.delta_stepping(len(indptr) - 1, indptr, col, val, s, delta,
+                                           threads=threads)
+        total_t += time.perf_counter() - t0
+        total_m += int(deg[np.isfinite(dist)].sum())
+    return total_t, total_m
+
+
+def reference_arm(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    from paper_1911_06895_b200 import graphs
+
+    threads = max(1, oracle.max_threads())
+    # Input synthesis: the same R-MAT as our arm.  On a GPU box the device
+    # generator builds it (input prep only -- the timed path is pure CPU);
+    # otherwise the identical host generator.
+    try:
+        from paper_1911_06895_b200 import DeviceGraph, _lib
+        if _lib.device_count() > 0:
+            g = DeviceGraph.rmat(args.scale, args.edge_factor, 1, 2, device=local)
+            indptr, col, val = g.download()
+            g.close()
+        else:
+            raise RuntimeError
+    except Exception:
+        h = graphs.rmat(args.scale, args.edge_factor, 1, 2)
+        indptr, col, val = h.indptr, h.col, h.val
+    col64 = col.astype(np.int64)
+    val64 = val.astype(np.float64)
+    pool = graphs.pick_sources(indptr, args.sources, seed=7)
+    for k in range(args.warmup):
+        run_cpu_oracle(indptr, col64, val64, [pool[k % len(pool)]], args.delta, threads)
+    secs, edges = run_cpu_oracle(indptr, col64, val64,
+                                 [pool[(args.warmup + k) % len(pool)] for k in range(args.steps)],
+                                 args.delta, threads)
+    value = edges / secs / 1e9
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded R-MAT, fp32-lattice weights)",
+        "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_delta{args.delta}",
+                   "sources_per_step": 1, "n": len(indptr) - 1, "nnz": int(indptr[-1])},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"1 source per step, full solve incl. split (reference "
+                                   f"algorithm restated in C, oracle/), {cpu_model()}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+
+    from paper_1911_06895_b200 import DeviceGraph, graphs
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        pg = dist
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    delta = args.delta
+
+    # ---- graph: generated on the device, CSR mirrored in pinned host memory
+    g = DeviceGraph.rmat(args.scale, args.edge_factor, 1, 2, device=local, stream=sptr)
+    n, nnz = g.n, g.nnz
+    indptr_h, col_h, val_h = g.download()
+    pin_indptr = torch.from_numpy(indptr_h).pin_memory()
+    pin_col = torch.from_numpy(col_h).pin_memory()
+    pin_val = torch.from_numpy(val_h).pin_memory()
+    pool = graphs.pick_sources(indptr_h, args.sources, seed=7)
+    # weak scaling: rank r takes sources r, r+ws, ... of the pool
+    mine = pool[rank::ws] if ws > 1 else pool
+
+    def batch(step):
+        return [mine[(step * args.batch + j) % len(mine)] for j in range(args.batch)]
+
+    info = g.prepare(delta)
+
+    # ---- device-resident timing (value)
+    launches_per_solve = 1
+    for w in range(args.warmup):
+        for s in batch(w):
+            g.solve(s, delta)
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if not args.no_clocks:
+        clocks.start()
+        time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    per_solve = []
+    m_tot = 0
+    balg_tot = 0
+    ev0.record(stream)
+    for k in range(args.steps):
+        for s in batch(args.warmup + k):
+            st = g.solve(s, delta)
+            per_solve.append(st.as_dict() | {"source": s})
+            m_tot += st.edges_reached
+            balg_tot += b_alg(st.edges_reached, st.reached, n)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop() if not args.no_clocks else {"sm_mhz": None, "sm_max_mhz": None, "reasons": []}
+    t_ms = ev0.elapsed_time(ev1)
+    if pg is not None:
+        t = torch.tensor([t_ms], device=f"cuda:{local}")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        t_ms = float(t.item())
+        m = torch.tensor([m_tot], dtype=torch.float64, device=f"cuda:{local}")
+        pg.all_reduce(m)
+        m_all = float(m.item())
+    else:
+        m_all = float(m_tot)
+    value = m_all / (t_ms * 1e-3) / 1e9
+    kern_ms = [p["kernel_ms"] for p in per_solve]
+    mean_kern = sum(kern_ms) / len(kern_ms)
+    balg_mean = balg_tot / len(per_solve)
+    peak, peak_kind = measured_peaks()
+    achieved = balg_mean / (mean_kern * 1e-3) / 1e9
+
+    # ---- delta sweep (informational)
+    sweep = {}
+    if args.sweep:
+        for d in (0.05, 0.25):
+            g.prepare(d)
+            ts, ms = 0.0, 0
+            for s in batch(0):
+                st = g.solve(s, d)
+                ts += st.kernel_ms
+                ms += st.edges_reached
+            sweep[str(d)] = {"gteps": ms / (ts * 1e-3) / 1e9, "kernel_ms_mean": ts / args.batch}
+        g.prepare(delta)
+
+    # ---- end to end through the public API with host buffers (e2e)
+    e2e = None
+    if not args.no_e2e:
+        idx_buf = torch.empty(n, dtype=torch.int64).pin_memory()
+        val_buf = torch.empty(n, dtype=torch.float64).pin_memory()
+        h2d = pin_indptr.numel() * 8 + pin_col.numel() * 4 + pin_val.numel() * 4
+        e2e_launch = 0
+
+        def e2e_step(step):
+            nonlocal e2e_launch
+            d2h = 0
+            m = 0
+            hg = DeviceGraph.from_csr(n, pin_indptr, pin_col, pin_val, device=local, stream=sptr)
+            e2e_launch += 3  # indptr check, column check, weight widening
+            for s in batch(step):
+                st = hg.solve(s, delta)  # first call also splits (prepare)
+                idx, vals = hg.result_sparse(out=(idx_buf.numpy(), val_buf.numpy()))
+                d2h += int(st.reached) * 16
+                m += st.edges_reached
+                e2e_launch += 4  # solver + compaction (count, scan, write)
+            e2e_launch += 4  # split: count, 2 scans, scatter
+            hg.close()
+            return d2h, m
+
+        e2e_step(0)
+        barrier()
+        torch.cuda.synchronize()
+        e2e_launch = 0
+        t0 = time.perf_counter()
+        d2h_tot, m_e2e = 0, 0
+        for k in range(args.steps):
+            d, m = e2e_step(args.warmup + k)
+            d2h_tot += d
+            m_e2e += m
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        if pg is not None:
+            t = torch.tensor([t_e2e], device=f"cuda:{local}")
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            t_e2e = float(t.item())
+            mm = torch.tensor([m_e2e], dtype=torch.float64, device=f"cuda:{local}")
+            pg.all_reduce(mm)
+            m_e2e = float(mm.item())
+        e2e = {"value": m_e2e / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h_tot // args.steps,
+               "ms_per_step": t_e2e / args.steps * 1e3,
+               "includes": "pinned H2D of the CSR, device split, batch solves, D2H of "
+                           "every SparseVector (indices int64 + values f64)"}
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        threads = max(1, oracle.max_threads())
+        secs, edges = run_cpu_oracle(indptr_h, col_h.astype(np.int64), val_h.astype(np.float64),
+                                     [mine[0]], delta, threads)
+        cpu = {"value": edges / secs / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"1 source ({mine[0]}) of the same R-MAT graph, full solve incl. "
+                         f"split, reference algorithm restated in C (oracle/) with OpenMP, "
+                         f"{secs:.1f}s, {cpu_model()}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": ws,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "u32 fixed-point (exact f64)" if info.dist_mode == 0 else "f64",
+            "data": "synthetic (seeded R-MAT, generated on device, fp32-lattice weights)",
+            "config": {
+                "workload": f"rmat{args.scale}_ef{args.edge_factor}_delta{delta}",
+                "n": n, "nnz": nnz, "nnz_light": int(info.nnz_light),
+                "nnz_heavy": int(info.nnz_heavy), "sources_per_step": args.batch,
+                "source_pool": args.sources, "parallelism": f"replicas{ws}",
+                "l2": "inputs larger than L2 (CSR %.1f GB)" % (nnz * 8 / 1e9),
+            },
+            "roofline": {
+                "bound": "hbm",
+                "achieved": achieved,
+                "peak": peak,
+                "unit": "GB/s",
+                "frac": achieved / peak,
+                "traffic": None,
+                "peak_kind": peak_kind,
+                "kernel": "ds::sssp_persistent_kernel<ModeFixed>",
+                "algorithmic_bytes_per_launch": balg_mean,
+                "mean_launch_ms": mean_kern,
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_solve * len(per_solve),
+            "clocks": clk,
+            "solver": {
+                "gteps_kernel": m_tot / (sum(kern_ms) * 1e-3) / 1e9,
+                "phases_mean": statistics.mean(p["inner_phases"] for p in per_solve),
+                "buckets_mean": statistics.mean(p["buckets_visited"] for p in per_solve),
+                "barriers_mean": statistics.mean(p["grid_barriers"] for p in per_solve),
+                "edges_scanned_over_m_r": sum(p["edges_scanned"] for p in per_solve)
+                / max(1, sum(p["edges_reached"] for p in per_solve)),
+                "reached_mean": statistics.mean(p["reached"] for p in per_solve),
+                "kernel_ms_min": min(kern_ms),
+                "kernel_ms_max": max(kern_ms),
+                "prepare_ms": info.prepare_ms,
+                "sweep": sweep,
+            },
+        }
+        print(json.dumps(line), flush=True)
+    g.close()
+    if pg is not None:
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -79,11 +79,12 @@ def lib():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(LIB):
+        path = os.environ.get("DS_LIB", LIB)
+        if not os.path.exists(path):
             raise ImportError(
-                f"{LIB} is missing: build it with `python -m paper_1911_06895_b200.build` "
+                f"{path} is missing: build it with `python -m paper_1911_06895_b200.build` "
                 "(the solver has no CPU fallback)")
-        L = ctypes.CDLL(LIB)
+        L = ctypes.CDLL(path)
         L.ds_graph_create.argtypes = [_i64, _i64, _vp, _vp, ctypes.c_int, _vp, ctypes.c_int,
                                       ctypes.c_int, _vp, ctypes.POINTER(_vp)]
         L.ds_graph_prepare.argtypes = [_vp, ctypes.c_double, ctypes.c_uint32,

@@ -8,11 +8,11 @@ namespace ds {
 
 // Block shape of every kernel in the persistent solver.
 constexpr int kThreads = 256;
-// capture: entries per thread / per tile (one tile = one decoupled-look-back unit)
+// capture: entries per thread / per tile (one tile = one packed reservation)
 constexpr int kCapItems = 4;
 constexpr int kCapTile = kThreads * kCapItems;
 // relax: edges per thread / per tile (one tile = one shared-memory staging unit)
-constexpr int kRelItems = 4;
+constexpr int kRelItems = 8;
 constexpr int kRelTile = kThreads * kRelItems;
 
 constexpr unsigned long long kMask48 = (1ull << 48) - 1;

@@ -107,9 +107,6 @@ struct ds_graph {
     long long* Rbase = nullptr;
     void* Rd = nullptr;
     unsigned* tile_start = nullptr;
-    unsigned long long* tflag = nullptr;
-    unsigned long long* tagg = nullptr;
-    unsigned long long* tinc = nullptr;
     Ctl* ctl = nullptr;
     Ctl* h_ctl = nullptr;  // pinned
     PrepStats* pstat = nullptr;
@@ -121,18 +118,18 @@ struct ds_graph {
     size_t cub_bytes = 0;
     // serials (stamps / look-back flags persist across solves)
     unsigned pser = 1, bser = 1;
-    unsigned long long sser = 1;
     // last result
     bool have_result = false;
     long long reached = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int grid_fixed = 0, grid_f64 = 0;
+    size_t persist_bytes = 0, max_window = 0;
 };
 
 static void free_all(ds_graph* g) {
     void* ptrs[] = {g->indptr, g->col,  g->w,     g->Lptr,  g->Hptr,       g->Ledges, g->Hedges,
                     g->dist,   g->fstamp, g->sstamp, g->F0,  g->F1,         g->S,      g->Rpre,
-                    g->Rbase,  g->Rd,   g->tile_start, g->tflag, g->tagg,   g->tinc,   g->ctl,
+                    g->Rbase,  g->Rd,   g->tile_start, g->ctl,
                     g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -412,10 +409,6 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaMalloc(&g->Rd, sizeof(unsigned long long) * n));
     const long long ntile_rel = g->nnz / kRelTile + 4;
     CK(cudaMalloc(&g->tile_start, sizeof(unsigned) * ntile_rel));
-    const long long ntile_cap = n / kCapTile + 4;
-    CK(cudaMalloc(&g->tflag, sizeof(unsigned long long) * ntile_cap));
-    CK(cudaMalloc(&g->tagg, 2 * sizeof(unsigned long long) * ntile_cap));
-    CK(cudaMalloc(&g->tinc, 2 * sizeof(unsigned long long) * ntile_cap));
     CK(cudaMalloc(&g->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&g->h_ctl, sizeof(Ctl)));
     CK(cudaMalloc(&g->pstat, sizeof(PrepStats)));
@@ -425,7 +418,6 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaMalloc(&g->Hptr, sizeof(long long) * (n + 1)));
     CK(cudaMemsetAsync(g->fstamp, 0, sizeof(unsigned) * n, g->stream));
     CK(cudaMemsetAsync(g->sstamp, 0, sizeof(unsigned) * n, g->stream));
-    CK(cudaMemsetAsync(g->tflag, 0, sizeof(unsigned long long) * ntile_cap, g->stream));
     CK(cudaEventCreate(&g->ev0));
     CK(cudaEventCreate(&g->ev1));
     int occ = 0;
@@ -437,6 +429,24 @@ static int alloc_scratch(ds_graph* g) {
     g->grid_f64 = (int)grid_blocks_for(g->nsm, occ);
     if (g->grid_fixed <= 0 || g->grid_f64 <= 0)
         return set_err(DS_ECUDA, "persistent solver kernel cannot be resident on this device");
+    // L2 set-aside for the distance array (opt-in: DS_L2_PERSIST=1; measured
+    // slower than plain LRU + evict_first edge streaming on R-MAT 24)
+    const char* ps = getenv("DS_L2_PERSIST");
+    if (ps && atoi(ps) != 0) {
+        int maxp = 0, maxw = 0;
+        if (cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, g->device) == cudaSuccess &&
+            cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, g->device) == cudaSuccess &&
+            maxp > 0 && maxw > 0) {
+            size_t want = std::min((size_t)maxp, sizeof(unsigned long long) * (size_t)g->n);
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            g->persist_bytes = cur;
+            g->max_window = (size_t)maxw;
+        }
+        cudaGetLastError();
+    }
     return DS_OK;
 }
 
@@ -475,6 +485,7 @@ extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, co
     if (n < 1) return set_err(DS_EINVAL, "matrix dimension must be positive, got %lld", (long long)n);
     if (n > 0x7FFFFFFFLL) return set_err(DS_EINVAL, "vertex count %lld exceeds int32 ids", (long long)n);
     if (nnz < 0) return set_err(DS_EINVAL, "negative nnz");
+    if (nnz >= (1LL << 33)) return set_err(DS_EINVAL, "nnz %lld exceeds 2^33 edges", (long long)nnz);
     if (nnz > 0 && (!indptr || !col || !val)) return set_err(DS_EINVAL, "null CSR array");
     if (!indptr) return set_err(DS_EINVAL, "null indptr");
     if (col_dtype != DS_IDX_I32 && col_dtype != DS_IDX_I64)
@@ -710,20 +721,37 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     p.Rbase = g->Rbase;
     p.Rd = (typename M::D*)g->Rd;
     p.tile_start = g->tile_start;
-    p.tflag = g->tflag;
-    p.tagg = g->tagg;
-    p.tinc = g->tinc;
     p.ctl = g->ctl;
     p.out = g->out;
     p.pser0 = g->pser;
     p.bser0 = g->bser;
-    p.sser0 = g->sser;
     const unsigned grid = (unsigned)(std::is_same<M, ModeFixed>::value ? g->grid_fixed : g->grid_f64);
     CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
-    void* args[] = {(void*)&p};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = g->stream;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    int nattr = 1;
+    // keep the distance array L2-resident while edges stream through
+    const size_t dbytes = sizeof(typename M::D) * (size_t)g->n;
+    if (g->persist_bytes > 0) {
+        at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[1].val.accessPolicyWindow.base_ptr = g->dist;
+        at[1].val.accessPolicyWindow.num_bytes = std::min(dbytes, g->max_window);
+        at[1].val.accessPolicyWindow.hitRatio =
+            (float)std::min(1.0, (double)g->persist_bytes / (double)at[1].val.accessPolicyWindow.num_bytes);
+        at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        nattr = 2;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = nattr;
     CK(cudaEventRecord(g->ev0, g->stream));
-    CK(cudaLaunchCooperativeKernel((const void*)sssp_persistent_kernel<M>, dim3(grid), dim3(kThreads),
-                                   args, 0, g->stream));
+    CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M>, p));
     CK(cudaEventRecord(g->ev1, g->stream));
     CK(cudaMemcpyAsync(g->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
@@ -731,7 +759,6 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     // advance serials past everything this launch used
     g->pser += (unsigned)(c.phases + 4);
     g->bser += (unsigned)(c.visited + c.phases + 4);
-    g->sser += c.steps + 4;
     if (g->pser > 0x7FFFFFFFu || g->bser > 0x7FFFFFFFu) {
         CK(cudaMemsetAsync(g->fstamp, 0, sizeof(unsigned) * g->n, g->stream));
         CK(cudaMemsetAsync(g->sstamp, 0, sizeof(unsigned) * g->n, g->stream));

@@ -24,11 +24,17 @@
 //    non-skip outer_iterations is recovered on the host from max(t_final).
 //
 // Work decomposition per step (all steps grid-stride over the persistent grid):
-//  capture : frontier ids -> (captured d, row offset, degree) entries with a
-//            single-pass decoupled look-back scan over degrees; also writes a
-//            tile->first-entry map so the relax step needs no search in HBM.
+//  capture : frontier ids -> (captured d, row base, degree prefix) entries.
+//            Each CTA tile scans its degrees in shared memory and reserves
+//            its (entries, edges) ranges with ONE packed 64-bit atomicAdd, so
+//            entry ranks and edge prefixes stay consistent without a global
+//            scan; it also writes a tile->first-entry map for the relax step.
 //  relax   : edge-balanced; each CTA stages one tile's entries in shared
-//            memory, each thread walks kRelItems consecutive virtual edges.
+//            memory, each thread maps kRelItems consecutive virtual edges to
+//            their rows, then issues all edge loads, all distance loads and
+//            finally the atomicMin pushes (three batched latency stages).
+//  Appends (next frontier, S) are staged in a per-CTA shared-memory queue and
+//  flushed with one global atomic per tile.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -50,7 +56,13 @@ struct ModeFixed {
     using D = unsigned;
     using Edge = uint2;  // x = column, y = weight * 2^frac
     static constexpr D INF = 0xFFFFFFFFu;
-    __device__ __forceinline__ static Edge load(const Edge* p) { return __ldg(p); }
+    __device__ __forceinline__ static Edge load(const Edge* p, unsigned long long pol) {
+        Edge r;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+                     : "=r"(r.x), "=r"(r.y)
+                     : "l"(p), "l"(pol));
+        return r;
+    }
     __device__ __forceinline__ static unsigned col(const Edge& e) { return e.x; }
     __device__ __forceinline__ static bool add(D du, const Edge& e, D& nd) {
         unsigned long long s = (unsigned long long)du + e.y;
@@ -80,8 +92,11 @@ struct ModeF64 {
     using D = unsigned long long;
     using Edge = EdgeF64;
     static constexpr D INF = 0x7FF0000000000000ull;
-    __device__ __forceinline__ static Edge load(const Edge* p) {
-        uint4 q = __ldg(reinterpret_cast<const uint4*>(p));
+    __device__ __forceinline__ static Edge load(const Edge* p, unsigned long long pol) {
+        uint4 q;
+        asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w)
+                     : "l"(p), "l"(pol));
         Edge e;
         e.col = q.x;
         e.pad = 0;
@@ -104,16 +119,17 @@ struct ModeF64 {
 
 // ---------------------------------------------------------------- control block
 
+constexpr int kPackShift = 33;  // capture reservation: (entries << 33) | edges
+constexpr unsigned long long kMask33 = (1ull << kPackShift) - 1;
+
 struct StepSlot {
-    unsigned long long tile_claim;
+    unsigned long long re_packed;     // capture: reserved (entries << 33) | edges
     unsigned long long front_count;   // capture (range mode): frontier size
-    unsigned long long rcount;        // capture: entries with degree > 0
-    unsigned long long etotal;        // capture: total degree
     unsigned long long next_min;      // capture (range mode): min D >= H
     unsigned long long append_count;  // relax (light): next-frontier size
     unsigned int flags;               // bit0: fixed-point overflow
     unsigned int pad;
-    unsigned long long pad2;
+    unsigned long long pad2[3];
 };
 
 struct Ctl {
@@ -156,14 +172,12 @@ struct KParams {
     long long* Rbase;
     D* Rd;
     unsigned* tile_start;
-    unsigned long long* tflag;
-    unsigned long long* tagg;  // 2 per tile: (count, degree)
-    unsigned long long* tinc;  // 2 per tile: inclusive prefix
     Ctl* ctl;
     double* out;
     unsigned pser0, bser0;
-    unsigned long long sser0;
 };
+
+constexpr int kQCap = 1024;  // per-CTA append staging (overflow spills to global)
 
 template <class D>
 struct SmemRelax {
@@ -180,9 +194,12 @@ struct Smem {
         SmemRelax<D> rx;
         typename BlockScanU64::TempStorage scan;
     } u;
+    int qbuf[kQCap];
+    unsigned qcnt;
+    unsigned qn;
+    unsigned long long qbase;
     unsigned long long red[kThreads / 32];
     unsigned long long red2[kThreads / 32];
-    unsigned long long tile;
     unsigned long long pc, pd;
     int ok;
 };
@@ -212,8 +229,8 @@ __device__ __forceinline__ unsigned long long warp_max(unsigned long long v) {
 }
 
 // op: 0 sum, 1 min, 2 max; result valid in thread 0
-template <int OP, class S>
-__device__ __forceinline__ unsigned long long block_reduce(unsigned long long v, S& sm,
+template <int OP>
+__device__ __forceinline__ unsigned long long block_reduce(unsigned long long v,
                                                            unsigned long long* buf) {
     v = OP == 0 ? warp_sum(v) : OP == 1 ? warp_min(v) : warp_max(v);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -221,11 +238,16 @@ __device__ __forceinline__ unsigned long long block_reduce(unsigned long long v,
     if (lane == 0) buf[w] = v;
     __syncthreads();
     if (w == 0) {
-        v = lane < kThreads / 32 ? buf[lane]
-                                 : (OP == 1 ? ~0ull : 0ull);
+        v = lane < kThreads / 32 ? buf[lane] : (OP == 1 ? ~0ull : 0ull);
         v = OP == 0 ? warp_sum(v) : OP == 1 ? warp_min(v) : warp_max(v);
     }
     return v;
+}
+
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 
 // Grid-wide barrier over a co-resident (cooperative) grid.  Returns false if
@@ -267,13 +289,38 @@ __device__ __forceinline__ bool grid_sync(Ctl* c, unsigned& gen, unsigned long l
     return sm.ok != 0;
 }
 
-// Warp-aggregated append of v to list (divergence-safe).
-__device__ __forceinline__ void append_list(int* list, unsigned long long* counter, int v) {
+// Stage v in the CTA's shared-memory queue (warp-aggregated); spill straight
+// to the global list when the queue is full.
+template <class S>
+__device__ __forceinline__ void q_push(S& sm, int* list, unsigned long long* counter, int v) {
     cg::coalesced_group g = cg::coalesced_threads();
-    unsigned long long base = 0;
-    if (g.thread_rank() == 0) base = atomicAdd(counter, (unsigned long long)g.size());
-    base = g.shfl(base, 0);
-    list[base + g.thread_rank()] = v;
+    unsigned pos = 0;
+    if (g.thread_rank() == 0) pos = atomicAdd(&sm.qcnt, (unsigned)g.size());
+    pos = g.shfl(pos, 0) + g.thread_rank();
+    if (pos < (unsigned)kQCap) {
+        sm.qbuf[pos] = v;
+    } else {
+        cg::coalesced_group h = cg::coalesced_threads();
+        unsigned long long b = 0;
+        if (h.thread_rank() == 0) b = atomicAdd(counter, (unsigned long long)h.size());
+        b = h.shfl(b, 0);
+        list[b + h.thread_rank()] = v;
+    }
+}
+
+// Reserve global space for the staged queue (thread 0); call between two
+// __syncthreads, then q_copy after the second.
+template <class S>
+__device__ __forceinline__ void q_reserve(S& sm, unsigned long long* counter) {
+    const unsigned c = sm.qcnt < (unsigned)kQCap ? sm.qcnt : (unsigned)kQCap;
+    sm.qn = c;
+    sm.qbase = c ? atomicAdd(counter, (unsigned long long)c) : 0ull;
+    sm.qcnt = 0;
+}
+template <class S>
+__device__ __forceinline__ void q_copy(S& sm, int* list) {
+    const unsigned c = sm.qn;
+    for (unsigned i = threadIdx.x; i < c; i += kThreads) list[sm.qbase + i] = sm.qbuf[i];
 }
 
 // ---------------------------------------------------------------- capture step
@@ -281,150 +328,104 @@ __device__ __forceinline__ void append_list(int* list, unsigned long long* count
 // Input: a frontier given as an id list (LIST) or as "all vertices whose
 // distance lies in [L, H)" (RANGE: compute_bucket, sssp.py:153-158).
 // Output: compacted entries (captured d, row base, degree prefix) of the
-// frontier vertices with at least one edge in `ptr`'s CSR, the tile map, and
-// slot totals.  APPEND_S adds every frontier vertex to S (dedup by stamp).
+// frontier vertices with at least one edge in `ptr`'s CSR, the relax tile
+// map, and the slot totals.  APPEND_S adds every frontier vertex to S
+// (S = S + t_Bi, sssp.py:191; dedup by the bucket stamp).
 
 template <class M, bool RANGE, bool APPEND_S>
 __device__ void capture_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
-                             unsigned long long ser, const int* list, unsigned long long count,
-                             typename M::D L, typename M::D H, const long long* ptr,
-                             unsigned bser, unsigned long long* s_counter, unsigned& gen,
-                             unsigned long long deadline) {
+                             const int* list, unsigned long long count, typename M::D L,
+                             typename M::D H, const long long* ptr, unsigned bser,
+                             unsigned long long* s_counter) {
     using D = typename M::D;
     const unsigned long long total = RANGE ? (unsigned long long)p.n : count;
     const unsigned long long ntiles = (total + kCapTile - 1) / kCapTile;
     unsigned long long local_fc = 0;
     unsigned long long local_min = ~0ull;
 
-    for (;;) {
-        if (threadIdx.x == 0) sm.tile = atomicAdd(&slot->tile_claim, 1ull);
-        __syncthreads();
-        const unsigned long long tile = sm.tile;
-        if (tile >= ntiles) break;
-
+    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        __syncthreads();  // shared queue / scan storage reuse across tiles
         const unsigned long long base = tile * kCapTile + (unsigned long long)threadIdx.x * kCapItems;
         int vtx[kCapItems];
         D dv[kCapItems];
-        long long off[kCapItems];
-        long long deg[kCapItems];
-        unsigned long long packed = 0;  // (count << 48) | degree
+        bool in[kCapItems];
 #pragma unroll
         for (int j = 0; j < kCapItems; ++j) {
-            deg[j] = 0;
-            vtx[j] = 0;
-            dv[j] = 0;
-            off[j] = 0;
             const unsigned long long idx = base + j;
-            if (idx < total) {
-                const int v = RANGE ? (int)idx : ldcg(list + idx);
-                const D d = __ldcg(p.dist + v);
-                bool in = true;
-                if (RANGE) {
-                    in = (d >= L) && (d < H);
-                    if (d >= H && d != M::INF && (unsigned long long)d < local_min)
-                        local_min = (unsigned long long)d;
+            in[j] = idx < total;
+            vtx[j] = in[j] ? (RANGE ? (int)idx : ldcg(list + idx)) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kCapItems; ++j) dv[j] = in[j] ? __ldcg(p.dist + vtx[j]) : M::INF;
+        long long off[kCapItems];
+        long long deg[kCapItems];
+        unsigned long long packed = 0;  // (count << 48) | degree within the tile
+#pragma unroll
+        for (int j = 0; j < kCapItems; ++j) {
+            if (RANGE && in[j]) {
+                const D d = dv[j];
+                if (d >= H && d != M::INF && (unsigned long long)d < local_min)
+                    local_min = (unsigned long long)d;
+                in[j] = (d >= L) && (d < H);
+            }
+            off[j] = in[j] ? __ldg(ptr + vtx[j]) : 0;
+            deg[j] = in[j] ? __ldg(ptr + vtx[j] + 1) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kCapItems; ++j) {
+            if (in[j]) {
+                ++local_fc;
+                if (APPEND_S) {
+                    if (atomicExch(p.sstamp + vtx[j], bser) != bser) q_push(sm, p.S, s_counter, vtx[j]);
                 }
-                if (in) {
-                    ++local_fc;
-                    if (APPEND_S) {
-                        if (atomicExch(p.sstamp + v, bser) != bser) append_list(p.S, s_counter, v);
-                    }
-                    const long long o = __ldg(ptr + v);
-                    const long long dg = __ldg(ptr + v + 1) - o;
-                    vtx[j] = v;
-                    dv[j] = d;
-                    off[j] = o;
-                    deg[j] = dg;
-                    if (dg > 0) packed += (1ull << 48) + (unsigned long long)dg;
-                }
+                deg[j] -= off[j];
+                if (deg[j] > 0) packed += (1ull << 48) + (unsigned long long)deg[j];
+            } else {
+                deg[j] = 0;
             }
         }
         unsigned long long excl, agg;
         BlockScanU64(sm.u.scan).ExclusiveSum(packed, excl, agg);
-
+        __syncthreads();
         if (threadIdx.x == 0) {
-            bool aborted = false;
-            // decoupled look-back over this step's tiles (single pass)
-            const unsigned long long ac = agg >> 48, ad = agg & kMask48;
-            unsigned long long ec = 0, ed = 0;
-            if (tile == 0) {
-                p.tinc[0] = ac;
-                p.tinc[1] = ad;
-                __threadfence();
-                st_release_u64(p.tflag, (ser << 2) | 2ull);
-            } else {
-                p.tagg[2 * tile] = ac;
-                p.tagg[2 * tile + 1] = ad;
-                __threadfence();
-                st_release_u64(p.tflag + tile, (ser << 2) | 1ull);
-                long long t = (long long)tile - 1;
-                unsigned spins = 0;
-                for (;;) {
-                    const unsigned long long f = ld_acquire_u64(p.tflag + t);
-                    if ((f >> 2) != ser) {
-                        if ((++spins & 1023u) == 0) {
-                            if (ld_acquire_u32(&p.ctl->abort)) {
-                                aborted = true;
-                                break;
-                            }
-                            if (globaltimer_ns() > deadline) {
-                                atomicExch(&p.ctl->abort, 1u);
-                                aborted = true;
-                                break;
-                            }
-                        }
-                        continue;
-                    }
-                    if ((f & 3ull) == 2ull) {
-                        ec += ldcg(p.tinc + 2 * t);
-                        ed += ldcg(p.tinc + 2 * t + 1);
-                        break;
-                    }
-                    ec += ldcg(p.tagg + 2 * t);
-                    ed += ldcg(p.tagg + 2 * t + 1);
-                    --t;
-                }
-                p.tinc[2 * tile] = ec + ac;
-                p.tinc[2 * tile + 1] = ed + ad;
-                __threadfence();
-                st_release_u64(p.tflag + tile, (ser << 2) | 2ull);
+            // one packed reservation keeps entry ranks and edge prefixes in
+            // the same order across tiles
+            if (agg) {
+                const unsigned long long want = ((agg >> 48) << kPackShift) | (agg & kMask48);
+                const unsigned long long r = atomicAdd(&slot->re_packed, want);
+                sm.pc = r >> kPackShift;
+                sm.pd = r & kMask33;
             }
-            sm.pc = aborted ? ~0ull : ec;
-            sm.pd = ed;
-            if (!aborted && tile == ntiles - 1) {
-                slot->rcount = ec + ac;
-                slot->etotal = ed + ad;
-            }
+            if (APPEND_S) q_reserve(sm, s_counter);
         }
         __syncthreads();
-        if (sm.pc == ~0ull) break;  // watchdog abort: the next barrier exits
-        unsigned long long rank = sm.pc + (excl >> 48);
-        unsigned long long pre = sm.pd + (excl & kMask48);
+        if (APPEND_S) q_copy(sm, p.S);
+        if (agg) {
+            unsigned long long rank = sm.pc + (excl >> 48);
+            unsigned long long pre = sm.pd + (excl & kMask48);
 #pragma unroll
-        for (int j = 0; j < kCapItems; ++j) {
-            if (deg[j] > 0) {
-                p.Rpre[rank] = (long long)pre;
-                p.Rbase[rank] = off[j] - (long long)pre;
-                p.Rd[rank] = dv[j];
-                const unsigned long long t0 = (pre + kRelTile - 1) / kRelTile;
-                const unsigned long long t1 = (pre + (unsigned long long)deg[j] - 1) / kRelTile;
-                for (unsigned long long t = t0; t <= t1; ++t) p.tile_start[t] = (unsigned)rank;
-                ++rank;
-                pre += (unsigned long long)deg[j];
+            for (int j = 0; j < kCapItems; ++j) {
+                if (deg[j] > 0) {
+                    p.Rpre[rank] = (long long)pre;
+                    p.Rbase[rank] = off[j] - (long long)pre;
+                    p.Rd[rank] = dv[j];
+                    const unsigned long long t0 = (pre + kRelTile - 1) / kRelTile;
+                    const unsigned long long t1 = (pre + (unsigned long long)deg[j] - 1) / kRelTile;
+                    for (unsigned long long t = t0; t <= t1; ++t) p.tile_start[t] = (unsigned)rank;
+                    ++rank;
+                    pre += (unsigned long long)deg[j];
+                }
             }
-            (void)vtx[j];
         }
-        __syncthreads();  // sm.tile / sm.pc / scan storage reuse
     }
     if (RANGE) {
-        const unsigned long long fc = block_reduce<0>(local_fc, sm, sm.red);
-        const unsigned long long mn = block_reduce<1>(local_min, sm, sm.red2);
+        const unsigned long long fc = block_reduce<0>(local_fc, sm.red);
+        const unsigned long long mn = block_reduce<1>(local_min, sm.red2);
         if (threadIdx.x == 0) {
             if (fc) atomicAdd(&slot->front_count, fc);
             if (mn != ~0ull) atomicMin(&slot->next_min, mn);
         }
     }
-    (void)gen;
 }
 
 // ---------------------------------------------------------------- relax step
@@ -439,7 +440,9 @@ __device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
                            const typename M::Edge* edges, typename M::D H, int* out_list,
                            unsigned pser) {
     using D = typename M::D;
+    using Edge = typename M::Edge;
     const unsigned long long ntile = (E + kRelTile - 1) / kRelTile;
+    const unsigned long long pol = evict_first_policy();
     bool overflow = false;
     for (unsigned long long t = blockIdx.x; t < ntile; t += gridDim.x) {
         const unsigned long long r0 = ldcg(p.tile_start + t);
@@ -455,7 +458,8 @@ __device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
         }
         __syncthreads();
         const int rel0 = threadIdx.x * kRelItems;
-        if ((unsigned long long)(tb + rel0) < E) {
+        const long long left = (long long)E - (tb + rel0);  // edges this thread may own
+        if (left > 0) {
             int lo = 0, hi = ne;
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
@@ -463,30 +467,53 @@ __device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
                 else hi = mid;
             }
             int k = lo;
+            int kk[kRelItems];
+            Edge ed[kRelItems];
+            // stage 1: rows of my edges, then all edge loads (independent)
 #pragma unroll
             for (int j = 0; j < kRelItems; ++j) {
-                const int rel = rel0 + j;
-                const long long e = tb + rel;
-                if ((unsigned long long)e >= E) break;
-                while (k + 1 < ne && sm.u.rx.rel[k + 1] <= rel) ++k;
-                const typename M::Edge ed = M::load(edges + (sm.u.rx.base[k] + e));
-                D nd;
-                if (!M::add(sm.u.rx.d[k], ed, nd)) {
-                    overflow = true;
-                    continue;
+                while (k + 1 < ne && sm.u.rx.rel[k + 1] <= rel0 + j) ++k;
+                kk[j] = k;
+            }
+#pragma unroll
+            for (int j = 0; j < kRelItems; ++j)
+                if (j < left) ed[j] = M::load(edges + (sm.u.rx.base[kk[j]] + tb + rel0 + j), pol);
+            // stage 2: candidate distances and current values
+            D nd[kRelItems], cur[kRelItems];
+#pragma unroll
+            for (int j = 0; j < kRelItems; ++j) {
+                cur[j] = (D)0;
+                if (j < left) {
+                    if (M::add(sm.u.rx.d[kk[j]], ed[j], nd[j])) {
+                        cur[j] = __ldcg(p.dist + M::col(ed[j]));
+                    } else {
+                        overflow = true;
+                    }
                 }
-                const unsigned v = M::col(ed);
-                const D cur = __ldcg(p.dist + v);
-                if (nd < cur) {
-                    const D old = atomicMin(p.dist + v, nd);
-                    if (LIGHT && nd < old && nd < H) {
-                        if (atomicExch(p.fstamp + v, pser) != pser)
-                            append_list(out_list, &slot->append_count, (int)v);
+            }
+            // stage 3: pushes
+#pragma unroll
+            for (int j = 0; j < kRelItems; ++j) {
+                if (j < left && nd[j] < cur[j]) {
+                    const unsigned v = M::col(ed[j]);
+                    if (LIGHT) {
+                        const D old = atomicMin(p.dist + v, nd[j]);
+                        if (nd[j] < old && nd[j] < H) {
+                            if (atomicExch(p.fstamp + v, pser) != pser)
+                                q_push(sm, out_list, &slot->append_count, (int)v);
+                        }
+                    } else {
+                        atomicMin(p.dist + v, nd[j]);
                     }
                 }
             }
         }
         __syncthreads();
+        if (LIGHT) {
+            if (threadIdx.x == 0) q_reserve(sm, &slot->append_count);
+            __syncthreads();
+            q_copy(sm, out_list);
+        }
     }
     if (overflow) atomicOr(&slot->flags, 1u);
 }
@@ -494,14 +521,17 @@ __device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
 // ---------------------------------------------------------------- the solver
 
 template <class M>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 3)
     sssp_persistent_kernel(const KParams<M> p) {
     using D = typename M::D;
     __shared__ Smem<D> sm;
     Ctl* const c = p.ctl;
     unsigned gen = 0;
     unsigned long long deadline = 0;
-    if (threadIdx.x == 0) deadline = globaltimer_ns() + p.timeout_ns;
+    if (threadIdx.x == 0) {
+        deadline = globaltimer_ns() + p.timeout_ns;
+        sm.qcnt = 0;
+    }
 
     // ---- init: t = {source: 0} (sssp.py:276), all else +inf
     {
@@ -511,8 +541,7 @@ __global__ void __launch_bounds__(kThreads)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             for (int k = 0; k < 3; ++k) {
                 StepSlot* s = &c->slot[k];
-                s->tile_claim = s->front_count = s->rcount = s->etotal = 0;
-                s->append_count = 0;
+                s->re_packed = s->front_count = s->append_count = 0;
                 s->flags = 0;
                 s->next_min = ~0ull;
             }
@@ -529,17 +558,13 @@ __global__ void __launch_bounds__(kThreads)
     int pp = 0;
     int status = 0;
 
-    auto reset_next = [&]() {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+    auto end_step = [&]() -> bool {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {  // recycle the slot two steps ahead
             StepSlot* s = &c->slot[(st + 1) % 3];
-            s->tile_claim = s->front_count = s->rcount = s->etotal = 0;
-            s->append_count = 0;
+            s->re_packed = s->front_count = s->append_count = 0;
             s->flags = 0;
             s->next_min = ~0ull;
         }
-    };
-    auto end_step = [&]() -> bool {
-        reset_next();
         const bool ok = grid_sync(c, gen, deadline, sm);
         ++st;
         ++nbar;
@@ -555,12 +580,11 @@ __global__ void __launch_bounds__(kThreads)
 
         // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
         if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[(bser & 1) ^ 1] = 0;
-        capture_step<M, true, true>(p, sm, &c->slot[st % 3], p.sser0 + st, nullptr, 0, L, H,
-                                    p.Lptr, bser, &c->s_count[bser & 1], gen, deadline);
+        capture_step<M, true, true>(p, sm, &c->slot[st % 3], nullptr, 0, L, H, p.Lptr, bser,
+                                    &c->s_count[bser & 1]);
         if (!end_step()) return;
-        unsigned long long fc = ldcg(&prev()->front_count);
-        unsigned long long E = ldcg(&prev()->etotal);
-        unsigned long long Rc = ldcg(&prev()->rcount);
+        const unsigned long long fc = ldcg(&prev()->front_count);
+        unsigned long long re = ldcg(&prev()->re_packed);
         if (fc == 0) {
             const unsigned long long nm = ldcg(&prev()->next_min);
             if (nm == ~0ull) break;  // nothing stored beyond: done
@@ -577,10 +601,11 @@ __global__ void __launch_bounds__(kThreads)
                 break;
             }
             unsigned long long nf = 0;
+            const unsigned long long E = re & kMask33;
             if (E > 0) {
                 escanned += E;
-                relax_step<M, true>(p, sm, &c->slot[st % 3], E, Rc, p.Ledges, H, pp ? p.F1 : p.F0,
-                                    pser);
+                relax_step<M, true>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Ledges, H,
+                                    pp ? p.F1 : p.F0, pser);
                 if (!end_step()) return;
                 if (ldcg(&prev()->flags) & 1u) {
                     status = kDevOverflow;
@@ -590,26 +615,25 @@ __global__ void __launch_bounds__(kThreads)
             }
             ++pser;
             if (nf == 0) break;
-            capture_step<M, false, true>(p, sm, &c->slot[st % 3], p.sser0 + st, pp ? p.F1 : p.F0,
-                                         nf, L, H, p.Lptr, bser, &c->s_count[bser & 1], gen,
-                                         deadline);
+            capture_step<M, false, true>(p, sm, &c->slot[st % 3], pp ? p.F1 : p.F0, nf, L, H,
+                                         p.Lptr, bser, &c->s_count[bser & 1]);
             if (!end_step()) return;
-            E = ldcg(&prev()->etotal);
-            Rc = ldcg(&prev()->rcount);
+            re = ldcg(&prev()->re_packed);
             pp ^= 1;
         }
         if (status) break;
 
         // ---- heavy relaxation from S with current t (sssp.py:218-227)
         const unsigned long long scount = ldcg(&c->s_count[bser & 1]);
-        capture_step<M, false, false>(p, sm, &c->slot[st % 3], p.sser0 + st, p.S, scount, L, H,
-                                      p.Hptr, bser, nullptr, gen, deadline);
+        capture_step<M, false, false>(p, sm, &c->slot[st % 3], p.S, scount, L, H, p.Hptr, bser,
+                                      nullptr);
         if (!end_step()) return;
-        E = ldcg(&prev()->etotal);
-        Rc = ldcg(&prev()->rcount);
+        re = ldcg(&prev()->re_packed);
+        const unsigned long long E = re & kMask33;
         if (E > 0) {
             escanned += E;
-            relax_step<M, false>(p, sm, &c->slot[st % 3], E, Rc, p.Hedges, H, nullptr, pser);
+            relax_step<M, false>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Hedges, H,
+                                 nullptr, pser);
             if (!end_step()) return;
             if (ldcg(&prev()->flags) & 1u) {
                 status = kDevOverflow;
@@ -642,9 +666,9 @@ __global__ void __launch_bounds__(kThreads)
             }
             p.out[v] = M::to_f64(d, p.frac);
         }
-        cnt = block_reduce<0>(cnt, sm, sm.red);
-        m = block_reduce<0>(m, sm, sm.red2);
-        mx = block_reduce<2>(mx, sm, sm.red);
+        cnt = block_reduce<0>(cnt, sm.red);
+        m = block_reduce<0>(m, sm.red2);
+        mx = block_reduce<2>(mx, sm.red);
         if (threadIdx.x == 0) {
             atomicAdd(&c->reached, cnt);
             atomicAdd(&c->edges_reached, m);
