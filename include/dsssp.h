@@ -124,6 +124,12 @@ void ds_graph_destroy(ds_graph* g);
 const char* ds_last_error(void);
 int ds_device_count(void);
 
+/* Debug timeline of the last solve when DS_TRACE=1 was set: out holds
+ * 1 + 2*cap words = [start_ns, then per grid step (end_ns, kind<<56 | work)]
+ * with kind 0 bucket scan, 1 light relax, 2 light capture, 3 heavy capture,
+ * 4 heavy relax.  Returns the number of steps written. */
+int64_t ds_debug_trace(ds_graph* g, uint64_t* out, int64_t cap);
+
 /* On-device synthetic R-MAT (Graph500 a,b,c,d = .57,.19,.19,.05; self-loops
  * dropped; symmetrised; deduplicated; fp32-lattice weight k*2^-24 per
  * undirected pair).  Bit-identical to paper_1911_06895_b200.graphs.rmat.

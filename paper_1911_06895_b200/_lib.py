@@ -22,7 +22,7 @@ DS_MODE_FIXED32, DS_MODE_F64 = 0, 1
 EXPORTS = (
     "ds_graph_create", "ds_graph_prepare", "ds_sssp", "ds_result_dense", "ds_result_sparse",
     "ds_export_split", "ds_graph_set_stream", "ds_graph_size", "ds_graph_destroy",
-    "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download",
+    "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download", "ds_debug_trace",
 )
 
 
@@ -102,6 +102,8 @@ def lib():
         L.ds_gen_rmat.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,
                                   ctypes.c_uint64, ctypes.c_int, _vp, ctypes.POINTER(_vp)]
         L.ds_graph_download.argtypes = [_vp, _vp, _vp, _vp]
+        L.ds_debug_trace.argtypes = [_vp, _vp, _i64]
+        L.ds_debug_trace.restype = _i64
         for name in ("ds_graph_create", "ds_graph_prepare", "ds_sssp", "ds_result_dense",
                      "ds_result_sparse", "ds_export_split", "ds_graph_set_stream",
                      "ds_graph_size", "ds_gen_rmat", "ds_graph_download"):

@@ -124,13 +124,17 @@ struct ds_graph {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int grid_fixed = 0, grid_f64 = 0;
     size_t persist_bytes = 0, max_window = 0;
+    unsigned long long* trace = nullptr;  // DS_TRACE=1: per-step timeline
+    unsigned long long trace_cap = 0;
+    unsigned long long trace_len = 0;
+    long long trace_t0 = 0;
 };
 
 static void free_all(ds_graph* g) {
     void* ptrs[] = {g->indptr, g->col,  g->w,     g->Lptr,  g->Hptr,       g->Ledges, g->Hedges,
                     g->dist,   g->fstamp, g->sstamp, g->F0,  g->F1,         g->S,      g->Rpre,
                     g->Rbase,  g->Rd,   g->tile_start, g->ctl,
-                    g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp};
+                    g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (g->h_ctl) cudaFreeHost(g->h_ctl);
@@ -421,11 +425,16 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaEventCreate(&g->ev0));
     CK(cudaEventCreate(&g->ev1));
     int occ = 0;
+    CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeFixed>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<unsigned>)));
+    CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeF64>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)sizeof(Smem<unsigned long long>)));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeFixed>,
-                                                     kThreads, 0));
+                                                     kThreads, sizeof(Smem<unsigned>)));
     g->grid_fixed = (int)grid_blocks_for(g->nsm, occ);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeF64>,
-                                                     kThreads, 0));
+                                                     kThreads, sizeof(Smem<unsigned long long>)));
     g->grid_f64 = (int)grid_blocks_for(g->nsm, occ);
     if (g->grid_fixed <= 0 || g->grid_f64 <= 0)
         return set_err(DS_ECUDA, "persistent solver kernel cannot be resident on this device");
@@ -723,6 +732,14 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     p.tile_start = g->tile_start;
     p.ctl = g->ctl;
     p.out = g->out;
+    if (const char* tr = getenv("DS_TRACE")) {
+        if (atoi(tr) && !g->trace) {
+            g->trace_cap = 1 << 20;
+            CK(cudaMalloc(&g->trace, 2 * sizeof(unsigned long long) * g->trace_cap));
+        }
+    }
+    p.trace = g->trace;
+    p.trace_cap = g->trace_cap;
     p.pser0 = g->pser;
     p.bser0 = g->bser;
     const unsigned grid = (unsigned)(std::is_same<M, ModeFixed>::value ? g->grid_fixed : g->grid_f64);
@@ -730,7 +747,7 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = sizeof(Smem<typename M::D>);
     cfg.stream = g->stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
@@ -765,6 +782,10 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
         g->pser = g->bser = 1;
     }
     if (c.abort) return set_err(DS_ETIMEOUT, "solver watchdog expired (DS_TIMEOUT_S=%g)", tmo);
+    if (g->trace) {
+        g->trace_len = std::min(c.steps, g->trace_cap);
+        g->trace_t0 = c.last_bucket;
+    }
     *dev_status = c.status;
     return DS_OK;
 }
@@ -971,3 +992,15 @@ int ds_internal_adopt(ds_graph** out, int device, void* stream, long long n, lon
 }
 
 int ds_internal_set_err(int code, const char* msg) { return set_err(code, "%s", msg); }
+
+extern "C" int64_t ds_debug_trace(ds_graph* g, uint64_t* out, int64_t cap) {
+    // out: 1 + 2*cap words = [t_start_ns, (t_ns, kind<<56 | work) per step]
+    if (!g || !g->trace || cap <= 0) return 0;
+    DeviceGuard guard(g->device);
+    const long long m = std::min((long long)g->trace_len, (long long)cap);
+    out[0] = (uint64_t)g->trace_t0;
+    if (m > 0 && cudaMemcpy(out + 1, g->trace, 2 * sizeof(unsigned long long) * m,
+                            cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    return m;
+}

@@ -174,6 +174,8 @@ struct KParams {
     unsigned* tile_start;
     Ctl* ctl;
     double* out;
+    unsigned long long* trace;  // optional per-step timeline (2 words / step)
+    unsigned long long trace_cap;
     unsigned pser0, bser0;
 };
 
@@ -184,6 +186,7 @@ struct SmemRelax {
     long long base[kRelTile + 1];
     D d[kRelTile + 1];
     int rel[kRelTile + 1];
+    unsigned short row[kRelTile];  // tile-local edge -> staged entry
 };
 
 using BlockScanU64 = cub::BlockScan<unsigned long long, kThreads>;
@@ -457,9 +460,10 @@ __device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
             sm.u.rx.d[k] = __ldcg(p.Rd + r);
         }
         __syncthreads();
-        const int rel0 = threadIdx.x * kRelItems;
-        const long long left = (long long)E - (tb + rel0);  // edges this thread may own
-        if (left > 0) {
+        // row map: thread t resolves the staged entry of tile edges
+        // [8t, 8t+8) with one binary search and a short walk
+        {
+            const int rel0 = threadIdx.x * kRelItems;
             int lo = 0, hi = ne;
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
@@ -467,23 +471,31 @@ __device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
                 else hi = mid;
             }
             int k = lo;
-            int kk[kRelItems];
-            Edge ed[kRelItems];
-            // stage 1: rows of my edges, then all edge loads (independent)
 #pragma unroll
             for (int j = 0; j < kRelItems; ++j) {
                 while (k + 1 < ne && sm.u.rx.rel[k + 1] <= rel0 + j) ++k;
-                kk[j] = k;
+                sm.u.rx.row[rel0 + j] = (unsigned short)k;
             }
+        }
+        __syncthreads();
+        // edges are taken lane-strided (edge = tb + tid + 256 j) so every warp
+        // load instruction reads 32 consecutive (col, w) pairs
+        const long long left = (long long)E - tb - threadIdx.x;  // > 256 j  <=>  edge j exists
+        if (left > 0) {
+            int kk[kRelItems];
+            Edge ed[kRelItems];
 #pragma unroll
-            for (int j = 0; j < kRelItems; ++j)
-                if (j < left) ed[j] = M::load(edges + (sm.u.rx.base[kk[j]] + tb + rel0 + j), pol);
+            for (int j = 0; j < kRelItems; ++j) {
+                const int r = threadIdx.x + j * kThreads;
+                kk[j] = sm.u.rx.row[r];
+                if (j * kThreads < left) ed[j] = M::load(edges + (sm.u.rx.base[kk[j]] + tb + r), pol);
+            }
             // stage 2: candidate distances and current values
             D nd[kRelItems], cur[kRelItems];
 #pragma unroll
             for (int j = 0; j < kRelItems; ++j) {
                 cur[j] = (D)0;
-                if (j < left) {
+                if (j * kThreads < left) {
                     if (M::add(sm.u.rx.d[kk[j]], ed[j], nd[j])) {
                         cur[j] = __ldcg(p.dist + M::col(ed[j]));
                     } else {
@@ -494,7 +506,7 @@ __device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
             // stage 3: pushes
 #pragma unroll
             for (int j = 0; j < kRelItems; ++j) {
-                if (j < left && nd[j] < cur[j]) {
+                if (j * kThreads < left && nd[j] < cur[j]) {
                     const unsigned v = M::col(ed[j]);
                     if (LIGHT) {
                         const D old = atomicMin(p.dist + v, nd[j]);
@@ -524,7 +536,8 @@ template <class M>
 __global__ void __launch_bounds__(kThreads, 3)
     sssp_persistent_kernel(const KParams<M> p) {
     using D = typename M::D;
-    __shared__ Smem<D> sm;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
     Ctl* const c = p.ctl;
     unsigned gen = 0;
     unsigned long long deadline = 0;
@@ -549,6 +562,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         }
     }
     if (!grid_sync(c, gen, deadline, sm)) return;
+    if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) c->last_bucket = (long long)globaltimer_ns();
 
     unsigned long long st = 0;  // step counter (identical on every CTA)
     unsigned long long nbar = 1, escanned = 0;
@@ -558,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     int pp = 0;
     int status = 0;
 
-    auto end_step = [&]() -> bool {
+    auto end_step = [&](unsigned long long kind, unsigned long long work) -> bool {
         if (blockIdx.x == 0 && threadIdx.x == 0) {  // recycle the slot two steps ahead
             StepSlot* s = &c->slot[(st + 1) % 3];
             s->re_packed = s->front_count = s->append_count = 0;
@@ -566,6 +580,10 @@ __global__ void __launch_bounds__(kThreads, 3)
             s->next_min = ~0ull;
         }
         const bool ok = grid_sync(c, gen, deadline, sm);
+        if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && st < p.trace_cap) {
+            p.trace[2 * st] = globaltimer_ns();
+            p.trace[2 * st + 1] = (kind << 56) | (work & ((1ull << 56) - 1));
+        }
         ++st;
         ++nbar;
         return ok;
@@ -582,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[(bser & 1) ^ 1] = 0;
         capture_step<M, true, true>(p, sm, &c->slot[st % 3], nullptr, 0, L, H, p.Lptr, bser,
                                     &c->s_count[bser & 1]);
-        if (!end_step()) return;
+        if (!end_step(0, (unsigned long long)p.n)) return;
         const unsigned long long fc = ldcg(&prev()->front_count);
         unsigned long long re = ldcg(&prev()->re_packed);
         if (fc == 0) {
@@ -606,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 escanned += E;
                 relax_step<M, true>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Ledges, H,
                                     pp ? p.F1 : p.F0, pser);
-                if (!end_step()) return;
+                if (!end_step(1, E)) return;
                 if (ldcg(&prev()->flags) & 1u) {
                     status = kDevOverflow;
                     break;
@@ -617,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             if (nf == 0) break;
             capture_step<M, false, true>(p, sm, &c->slot[st % 3], pp ? p.F1 : p.F0, nf, L, H,
                                          p.Lptr, bser, &c->s_count[bser & 1]);
-            if (!end_step()) return;
+            if (!end_step(2, nf)) return;
             re = ldcg(&prev()->re_packed);
             pp ^= 1;
         }
@@ -627,14 +645,14 @@ __global__ void __launch_bounds__(kThreads, 3)
         const unsigned long long scount = ldcg(&c->s_count[bser & 1]);
         capture_step<M, false, false>(p, sm, &c->slot[st % 3], p.S, scount, L, H, p.Hptr, bser,
                                       nullptr);
-        if (!end_step()) return;
+        if (!end_step(3, scount)) return;
         re = ldcg(&prev()->re_packed);
         const unsigned long long E = re & kMask33;
         if (E > 0) {
             escanned += E;
             relax_step<M, false>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Hedges, H,
                                  nullptr, pser);
-            if (!end_step()) return;
+            if (!end_step(4, E)) return;
             if (ldcg(&prev()->flags) & 1u) {
                 status = kDevOverflow;
                 break;
@@ -679,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 c->edges_scanned = escanned;
                 c->barriers = nbar;
                 c->steps = st;
-                c->last_bucket = idx;
+                if (!p.trace) c->last_bucket = idx;
                 c->status = 0;
             }
         }
