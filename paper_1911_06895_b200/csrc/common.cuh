@@ -6,14 +6,15 @@
 
 namespace ds {
 
-// Block shape of every kernel in the persistent solver.
-constexpr int kThreads = 256;
-// capture: entries per thread / per tile (one tile = one packed reservation)
-constexpr int kCapItems = 4;
-constexpr int kCapTile = kThreads * kCapItems;
-// relax: edges per thread / per tile (one tile = one shared-memory staging unit)
-constexpr int kRelItems = 8;
-constexpr int kRelTile = kThreads * kRelItems;
+// Block shape of the persistent solver (warp-granular work inside; the block
+// size only sets how many CTAs arrive at each grid barrier).
+#ifndef DS_THREADS
+#define DS_THREADS 768
+#endif
+#ifndef DS_MIN_BLOCKS
+#define DS_MIN_BLOCKS (768 / DS_THREADS)
+#endif
+constexpr int kThreads = DS_THREADS;
 
 constexpr unsigned long long kMask48 = (1ull << 48) - 1;
 

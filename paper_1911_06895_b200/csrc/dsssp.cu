@@ -9,6 +9,7 @@
 // is allocated once per handle and reused by every solve.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -98,15 +99,32 @@ struct ds_graph {
     size_t Lcap = 0, Hcap = 0;
     // scratch
     void* dist = nullptr;  // 8n bytes (either mode)
-    unsigned* fstamp = nullptr;
-    unsigned* sstamp = nullptr;
+    unsigned* fbits = nullptr;  // 2 x ceil(n/32) words: next-frontier dedup
+    unsigned* sbits = nullptr;  // ceil(n/32) words: S dedup
+    long long nwords = 0;
     int* F0 = nullptr;
     int* F1 = nullptr;
-    int* S = nullptr;
+    void* Fv0 = nullptr;  // frontier values (8n bytes each)
+    void* Fv1 = nullptr;
+    int* S0 = nullptr;
+    int* S1 = nullptr;
+    void* req = nullptr;  // pull partial minima (8n bytes)
+    // pull schedules (per prepare) for the light and heavy CSRs
+    struct Plan {
+        int* rowid = nullptr;
+        long long* cptr = nullptr;
+        unsigned* chunk_row = nullptr;
+        int* span = nullptr;
+        long long n_nz = 0, nspan = 0, nnz = 0;
+    } planL, planH;
+    bool symmetric = false;
     long long* Rpre = nullptr;
     long long* Rbase = nullptr;
     void* Rd = nullptr;
-    unsigned* tile_start = nullptr;
+    unsigned* chunk_start = nullptr;
+    int* order = nullptr;  // solver id -> input id
+    int* perm = nullptr;   // input id -> solver id
+    long long n_active = 0;
     Ctl* ctl = nullptr;
     Ctl* h_ctl = nullptr;  // pinned
     PrepStats* pstat = nullptr;
@@ -116,8 +134,6 @@ struct ds_graph {
     unsigned long long* ccount = nullptr;
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
-    // serials (stamps / look-back flags persist across solves)
-    unsigned pser = 1, bser = 1;
     // last result
     bool have_result = false;
     long long reached = 0;
@@ -132,8 +148,10 @@ struct ds_graph {
 
 static void free_all(ds_graph* g) {
     void* ptrs[] = {g->indptr, g->col,  g->w,     g->Lptr,  g->Hptr,       g->Ledges, g->Hedges,
-                    g->dist,   g->fstamp, g->sstamp, g->F0,  g->F1,         g->S,      g->Rpre,
-                    g->Rbase,  g->Rd,   g->tile_start, g->ctl,
+                    g->dist,   g->fbits, g->sbits, g->F0,  g->F1,  g->Fv0, g->Fv1, g->S0, g->S1, g->req, g->Rpre,
+                    g->planL.rowid, g->planL.cptr, g->planL.chunk_row, g->planL.span,
+                    g->planH.rowid, g->planH.cptr, g->planH.chunk_row, g->planH.span,
+                    g->Rbase,  g->Rd,   g->chunk_start, g->order, g->perm, g->ctl,
                     g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -210,15 +228,18 @@ __device__ __forceinline__ bool light_w(double w, double delta) { return w > 0.0
 __device__ __forceinline__ bool heavy_w(double w, double delta) { return w > delta && w < CUDART_INF; }
 
 // warp per row: light/heavy counts, min light weight, fixed-point eligibility
+// Rows are visited in solver order: row r of the output is input row
+// order[r] (identity when order == nullptr), columns are renamed through perm.
 __global__ void k_split_count(long long n, const long long* indptr, const double* w, double delta,
-                              long long* Lcnt, long long* Hcnt, PrepStats* st) {
+                              const int* order, long long* Lcnt, long long* Hcnt, PrepStats* st) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     unsigned long long minL = ~0ull, maxw = 0, nl = 0, nh = 0;
     int frac = 0;
     for (long long r = warp; r < n; r += nwarps) {
-        const long long a = indptr[r], b = indptr[r + 1];
+        const long long o = order ? order[r] : r;
+        const long long a = indptr[o], b = indptr[o + 1];
         unsigned lc = 0, hc = 0;
         for (long long e = a + lane; e < b; e += 32) {
             const double x = __ldg(w + e);
@@ -274,14 +295,16 @@ __device__ __forceinline__ void put_edge(EdgeF64* out, long long i, int c, doubl
 // filter_matrix semantics, ops.py:158-176)
 template <class Edge>
 __global__ void k_split_scatter(long long n, const long long* indptr, const int* col,
-                                const double* w, double delta, int frac, const long long* Lptr,
-                                const long long* Hptr, Edge* Lout, Edge* Hout) {
+                                const double* w, double delta, int frac, const int* order,
+                                const int* perm, const long long* Lptr, const long long* Hptr,
+                                Edge* Lout, Edge* Hout) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const unsigned lt = (1u << lane) - 1u;
     for (long long r = warp; r < n; r += nwarps) {
-        const long long a = indptr[r], b = indptr[r + 1];
+        const long long o = order ? order[r] : r;
+        const long long a = indptr[o], b = indptr[o + 1];
         long long lb = Lptr[r], hb = Hptr[r];
         for (long long e0 = a; e0 < b; e0 += 32) {
             const long long e = e0 + lane;
@@ -290,6 +313,7 @@ __global__ void k_split_scatter(long long n, const long long* indptr, const int*
             if (e < b) {
                 x = __ldg(w + e);
                 c = __ldg(col + e);
+                if (perm) c = __ldg(perm + c);
             }
             const bool L = e < b && light_w(x, delta);
             const bool H = e < b && heavy_w(x, delta);
@@ -301,6 +325,108 @@ __global__ void k_split_scatter(long long n, const long long* indptr, const int*
             hb += __popc(mH);
         }
     }
+}
+
+// ---------------------------------------------------------------- relabeling
+//
+// The solver works on vertex ids sorted by total degree (descending; stable,
+// so ties keep input order): hub distances share cache lines and every vertex
+// that can ever be reached (in- or out-degree > 0) sits in [0, n_active), so
+// the randomly accessed part of the distance array is as small as the live
+// graph.  Results are mapped back to input ids when they are written out.
+
+__global__ void k_outdeg_key(const long long* indptr, long long n, unsigned* key, int* iota) {
+    for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n;
+         v += (long long)gridDim.x * blockDim.x) {
+        const long long d = indptr[v + 1] - indptr[v];
+        key[v] = d > 0x7FFFFFFFLL ? 0x7FFFFFFFu : (unsigned)d;
+        iota[v] = (int)v;
+    }
+}
+
+__global__ void k_indeg_key(const int* col, long long nnz, unsigned* key) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nnz;
+         e += (long long)gridDim.x * blockDim.x)
+        atomicAdd(key + col[e], 1u);
+}
+
+__global__ void k_invert_order(const int* order, const unsigned* skey, long long n, int* perm,
+                               long long* n_active) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+         r += (long long)gridDim.x * blockDim.x) {
+        perm[order[r]] = (int)r;
+        if (skey[r] > 0 && (r + 1 == n || skey[r + 1] == 0)) *n_active = r + 1;
+    }
+}
+
+// ---------------------------------------------------------------- pull plans / symmetry
+
+// rows with edges, in solver order (stable compaction by an inclusive scan)
+__global__ void k_nz_flags(const long long* ptr, long long n, long long* flags) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+         r += (long long)gridDim.x * blockDim.x)
+        flags[r] = ptr[r + 1] > ptr[r] ? 1 : 0;
+}
+
+__global__ void k_nz_scatter(const long long* ptr, long long n, const long long* pos, int* rowid,
+                             long long* cptr) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+         r += (long long)gridDim.x * blockDim.x) {
+        if (ptr[r + 1] > ptr[r]) {
+            const long long k = pos[r] - 1;
+            rowid[k] = (int)r;
+            cptr[k] = ptr[r];
+        }
+        if (r == n - 1) cptr[pos[r]] = ptr[n];
+    }
+}
+
+template <int CHUNK>
+__global__ void k_chunk_plan(const long long* cptr, long long n_nz, unsigned* chunk_row, int* span,
+                             unsigned long long* nspan) {
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n_nz;
+         k += (long long)gridDim.x * blockDim.x) {
+        const long long st = cptr[k], en = cptr[k + 1];
+        const long long c0 = (st + CHUNK - 1) / CHUNK, c1 = (en - 1) / CHUNK;
+        for (long long c = c0; c <= c1; ++c) chunk_row[c] = (unsigned)k;
+        if (st / CHUNK != (en - 1) / CHUNK) span[atomicAdd(nspan, 1ull)] = (int)k;
+        if (k == n_nz - 1) chunk_row[(en + CHUNK - 1) / CHUNK] = (unsigned)k;
+    }
+}
+
+// A^T == A test (the pull reads rows of A as columns of A^T): every row has
+// strictly increasing columns, and each (u, v, w) has a bit-identical (v, u, w).
+__global__ void k_check_symmetric(const long long* indptr, const int* col, const double* w,
+                                  long long n, int* bad) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long u = warp; u < n; u += nwarps) {
+        const long long a = indptr[u], b = indptr[u + 1];
+        for (long long e = a + lane; e < b; e += 32) {
+            const int v = col[e];
+            if (e + 1 < b && col[e + 1] <= v) {
+                atomicOr(bad, 1);
+                continue;
+            }
+            long long lo = indptr[v], hi = indptr[v + 1];
+            while (lo < hi) {  // binary search for u in row v
+                const long long mid = (lo + hi) >> 1;
+                if (col[mid] < u) lo = mid + 1;
+                else hi = mid;
+            }
+            if (lo >= indptr[v + 1] || col[lo] != u ||
+                __double_as_longlong(w[lo]) != __double_as_longlong(w[e]))
+                atomicOr(bad, 1);
+        }
+    }
+}
+
+template <class D>
+__global__ void k_fill(D* a, long long m, D v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+         i += (long long)gridDim.x * blockDim.x)
+        a[i] = v;
 }
 
 // ---------------------------------------------------------------- compaction
@@ -403,16 +529,26 @@ extern "C" int ds_graph_size(const ds_graph* g, int64_t* n, int64_t* nnz) {
 static int alloc_scratch(ds_graph* g) {
     const long long n = g->n;
     CK(cudaMalloc(&g->dist, sizeof(unsigned long long) * n));
-    CK(cudaMalloc(&g->fstamp, sizeof(unsigned) * n));
-    CK(cudaMalloc(&g->sstamp, sizeof(unsigned) * n));
+    g->nwords = n / 32 + 1;
+    CK(cudaMalloc(&g->fbits, 2 * sizeof(unsigned) * g->nwords));
+    CK(cudaMalloc(&g->sbits, sizeof(unsigned) * g->nwords));
     CK(cudaMalloc(&g->F0, sizeof(int) * n));
     CK(cudaMalloc(&g->F1, sizeof(int) * n));
-    CK(cudaMalloc(&g->S, sizeof(int) * n));
+    CK(cudaMalloc(&g->S0, sizeof(int) * n));
+    CK(cudaMalloc(&g->S1, sizeof(int) * n));
+    CK(cudaMalloc(&g->Fv0, sizeof(unsigned long long) * n));
+    CK(cudaMalloc(&g->Fv1, sizeof(unsigned long long) * n));
+    CK(cudaMalloc(&g->req, sizeof(unsigned long long) * n));
+    for (ds_graph::Plan* pl : {&g->planL, &g->planH}) {
+        CK(cudaMalloc(&pl->rowid, sizeof(int) * n));
+        CK(cudaMalloc(&pl->cptr, sizeof(long long) * (n + 1)));
+        CK(cudaMalloc(&pl->span, sizeof(int) * n));
+        CK(cudaMalloc(&pl->chunk_row, sizeof(unsigned) * (g->nnz / 256 + 4)));
+    }
     CK(cudaMalloc(&g->Rpre, sizeof(long long) * n));
     CK(cudaMalloc(&g->Rbase, sizeof(long long) * n));
     CK(cudaMalloc(&g->Rd, sizeof(unsigned long long) * n));
-    const long long ntile_rel = g->nnz / kRelTile + 4;
-    CK(cudaMalloc(&g->tile_start, sizeof(unsigned) * ntile_rel));
+    CK(cudaMalloc(&g->chunk_start, sizeof(unsigned) * (g->nnz / kChunk + 4)));
     CK(cudaMalloc(&g->ctl, sizeof(Ctl)));
     CK(cudaMallocHost(&g->h_ctl, sizeof(Ctl)));
     CK(cudaMalloc(&g->pstat, sizeof(PrepStats)));
@@ -420,8 +556,8 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaMalloc(&g->out, sizeof(double) * n));
     CK(cudaMalloc(&g->Lptr, sizeof(long long) * (n + 1)));
     CK(cudaMalloc(&g->Hptr, sizeof(long long) * (n + 1)));
-    CK(cudaMemsetAsync(g->fstamp, 0, sizeof(unsigned) * n, g->stream));
-    CK(cudaMemsetAsync(g->sstamp, 0, sizeof(unsigned) * n, g->stream));
+    CK(cudaMemsetAsync(g->fbits, 0, 2 * sizeof(unsigned) * g->nwords, g->stream));
+    CK(cudaMemsetAsync(g->sbits, 0, sizeof(unsigned) * g->nwords, g->stream));
     CK(cudaEventCreate(&g->ev0));
     CK(cudaEventCreate(&g->ev1));
     int occ = 0;
@@ -484,6 +620,94 @@ static int check_csr(ds_graph* g) {
     CK(cudaStreamSynchronize(g->stream));
     if (h) return set_err(DS_EINVAL, "indptr must start at 0, be non-decreasing and end at nnz");
     return DS_OK;
+}
+
+static int build_plan(ds_graph* g, const long long* ptr, long long nnz, ds_graph::Plan& pl) {
+    const long long n = g->n;
+    pl.nnz = nnz;
+    pl.n_nz = 0;
+    pl.nspan = 0;
+    if (nnz == 0) return DS_OK;
+    k_nz_flags<<<elementwise_grid(g), 256, 0, g->stream>>>(ptr, n, g->Rpre);
+    CK(cudaGetLastError());
+    int rc = inclusive_scan_i64(g, g->Rpre, g->Rbase, n);
+    if (rc) return rc;
+    k_nz_scatter<<<elementwise_grid(g), 256, 0, g->stream>>>(ptr, n, g->Rbase, pl.rowid, pl.cptr);
+    CK(cudaGetLastError());
+    long long n_nz = 0;
+    CK(cudaMemcpyAsync(&n_nz, g->Rbase + (n - 1), sizeof(long long), cudaMemcpyDeviceToHost, g->stream));
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(g->pstat);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    k_chunk_plan<kChunk><<<elementwise_grid(g), 256, 0, g->stream>>>(pl.cptr, n_nz, pl.chunk_row, pl.span,
+                                                                      cnt);
+    CK(cudaGetLastError());
+    unsigned long long ns = 0;
+    CK(cudaMemcpyAsync(&ns, cnt, sizeof(ns), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    pl.n_nz = n_nz;
+    pl.nspan = (long long)ns;
+    return DS_OK;
+}
+
+static int check_symmetric(ds_graph* g) {
+    int* bad = reinterpret_cast<int*>(g->pstat);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
+    if (g->nnz > 0)
+        k_check_symmetric<<<(unsigned)(g->nsm * 16), 256, 0, g->stream>>>(g->indptr, g->col, g->w, g->n,
+                                                                          bad);
+    CK(cudaGetLastError());
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    CK(cudaStreamSynchronize(g->stream));
+    g->symmetric = (h == 0);
+    return DS_OK;
+}
+
+static int compute_order(ds_graph* g) {
+    const long long n = g->n;
+    unsigned *key = nullptr, *skey = nullptr;
+    int* iota = nullptr;
+    long long* nact = nullptr;
+    int rc = DS_OK;
+    size_t bytes = 0;
+    auto done = [&](int code) {
+        if (key) cudaFree(key);
+        if (skey) cudaFree(skey);
+        if (iota) cudaFree(iota);
+        if (nact) cudaFree(nact);
+        return code;
+    };
+#define CKO(call)                                                                          \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return done(set_err(e_ == cudaErrorMemoryAllocation ? DS_ENOMEM : DS_ECUDA,     \
+                                "CUDA error %s at %s:%d", cudaGetErrorName(e_), __FILE__,  \
+                                __LINE__));                                                \
+    } while (0)
+    CKO(cudaMalloc(&g->order, sizeof(int) * n));
+    CKO(cudaMalloc(&g->perm, sizeof(int) * n));
+    CKO(cudaMalloc(&key, sizeof(unsigned) * n));
+    CKO(cudaMalloc(&skey, sizeof(unsigned) * n));
+    CKO(cudaMalloc(&iota, sizeof(int) * n));
+    CKO(cudaMalloc(&nact, sizeof(long long)));
+    CKO(cudaMemsetAsync(nact, 0, sizeof(long long), g->stream));
+    k_outdeg_key<<<elementwise_grid(g), 256, 0, g->stream>>>(g->indptr, n, key, iota);
+    if (g->nnz > 0) k_indeg_key<<<elementwise_grid(g), 256, 0, g->stream>>>(g->col, g->nnz, key);
+    CKO(cudaGetLastError());
+    CKO(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, key, skey, iota, g->order, n, 0, 32,
+                                                  g->stream));
+    rc = ensure_cub(g, bytes);
+    if (rc) return done(rc);
+    CKO(cub::DeviceRadixSort::SortPairsDescending(g->cub_tmp, bytes, key, skey, iota, g->order, n, 0,
+                                                  32, g->stream));
+    k_invert_order<<<elementwise_grid(g), 256, 0, g->stream>>>(g->order, skey, n, g->perm, nact);
+    CKO(cudaGetLastError());
+    CKO(cudaMemcpyAsync(&g->n_active, nact, sizeof(long long), cudaMemcpyDeviceToHost, g->stream));
+    CKO(cudaStreamSynchronize(g->stream));
+#undef CKO
+    return done(DS_OK);
 }
 
 extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, const void* col,
@@ -590,6 +814,8 @@ extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, co
     CKG(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
     CKG(cudaStreamSynchronize(g->stream));
     if (h & 2) return fail(set_err(DS_EINVAL, "column index out of range for dimension %lld", (long long)n));
+    if ((rc = compute_order(g))) return fail(rc);
+    if ((rc = check_symmetric(g))) return fail(rc);
 #undef CKG
     *out = g;
     return DS_OK;
@@ -631,7 +857,8 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     CK(cudaMemsetAsync(g->Hptr, 0, sizeof(long long), g->stream));
     // per-row counts into scratch (Rpre / Rbase are n-sized int64)
     const unsigned grid = (unsigned)(g->nsm * 16);
-    k_split_count<<<grid, 256, 0, g->stream>>>(n, g->indptr, g->w, delta, g->Rpre, g->Rbase, g->pstat);
+    k_split_count<<<grid, 256, 0, g->stream>>>(n, g->indptr, g->w, delta, g->order, g->Rpre, g->Rbase,
+                                               g->pstat);
     CK(cudaGetLastError());
     int rc = inclusive_scan_i64(g, g->Rpre, g->Lptr + 1, n);
     if (rc) return rc;
@@ -670,12 +897,23 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     if ((rc = ensure_edges(&g->Hedges, &g->Hcap, esz * (size_t)g->nH))) return rc;
     if (mode == DS_MODE_FIXED32)
         k_split_scatter<uint2><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, delta, g->frac,
-                                                            g->Lptr, g->Hptr, (uint2*)g->Ledges,
-                                                            (uint2*)g->Hedges);
+                                                            g->order, g->perm, g->Lptr, g->Hptr,
+                                                            (uint2*)g->Ledges, (uint2*)g->Hedges);
     else
         k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, delta, 0,
-                                                              g->Lptr, g->Hptr, (EdgeF64*)g->Ledges,
+                                                              g->order, g->perm, g->Lptr, g->Hptr,
+                                                              (EdgeF64*)g->Ledges,
                                                               (EdgeF64*)g->Hedges);
+    CK(cudaGetLastError());
+    if (g->symmetric) {  // pull schedules (A^T == A: rows serve as columns)
+        if ((rc = build_plan(g, g->Lptr, g->nL, g->planL))) return rc;
+        if ((rc = build_plan(g, g->Hptr, g->nH, g->planH))) return rc;
+    }
+    if (mode == DS_MODE_FIXED32)
+        k_fill<unsigned><<<elementwise_grid(g), 256, 0, g->stream>>>((unsigned*)g->req, g->n, ModeFixed::INF);
+    else
+        k_fill<unsigned long long><<<elementwise_grid(g), 256, 0, g->stream>>>(
+            (unsigned long long*)g->req, g->n, ModeF64::INF);
     CK(cudaGetLastError());
     CK(cudaEventRecord(g->ev1, g->stream));
     CK(cudaStreamSynchronize(g->stream));
@@ -721,15 +959,34 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     p.Hptr = g->Hptr;
     p.Hedges = (const typename M::Edge*)g->Hedges;
     p.dist = (typename M::D*)g->dist;
-    p.fstamp = g->fstamp;
-    p.sstamp = g->sstamp;
-    p.F0 = g->F0;
-    p.F1 = g->F1;
-    p.S = g->S;
+    p.fbits[0] = g->fbits;
+    p.fbits[1] = g->fbits + g->nwords;
+    p.sbits = g->sbits;
+    p.F[0] = g->F0;
+    p.F[1] = g->F1;
+    p.Fv[0] = (typename M::D*)g->Fv0;
+    p.Fv[1] = (typename M::D*)g->Fv1;
+    p.S[0] = g->S0;
+    p.S[1] = g->S1;
+    p.req = (typename M::D*)g->req;
+    p.Lpull = {g->planL.rowid, g->planL.cptr, g->planL.chunk_row, g->planL.span, g->planL.n_nz,
+               g->planL.nspan, g->planL.nnz};
+    p.Hpull = {g->planH.rowid, g->planH.cptr, g->planH.chunk_row, g->planH.span, g->planH.n_nz,
+               g->planH.nspan, g->planH.nnz};
+    {
+        const char* e = getenv("DS_PULL");
+        p.pull_enabled = g->symmetric && !(e && atoi(e) == 0);
+        const char* a = getenv("DS_PULL_L");
+        const char* b = getenv("DS_PULL_H");
+        p.pull_light = a ? (float)atof(a) : 0.5f;
+        p.pull_heavy = b ? (float)atof(b) : 4.0f;  // heavy pull measured slower: off
+    }
     p.Rpre = g->Rpre;
     p.Rbase = g->Rbase;
     p.Rd = (typename M::D*)g->Rd;
-    p.tile_start = g->tile_start;
+    p.chunk_start = g->chunk_start;
+    p.perm = g->perm;
+    p.n_active = g->n_active;
     p.ctl = g->ctl;
     p.out = g->out;
     if (const char* tr = getenv("DS_TRACE")) {
@@ -740,8 +997,6 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     }
     p.trace = g->trace;
     p.trace_cap = g->trace_cap;
-    p.pser0 = g->pser;
-    p.bser0 = g->bser;
     const unsigned grid = (unsigned)(std::is_same<M, ModeFixed>::value ? g->grid_fixed : g->grid_f64);
     CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
     cudaLaunchConfig_t cfg = {};
@@ -773,13 +1028,11 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     CK(cudaMemcpyAsync(g->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
     const Ctl& c = *g->h_ctl;
-    // advance serials past everything this launch used
-    g->pser += (unsigned)(c.phases + 4);
-    g->bser += (unsigned)(c.visited + c.phases + 4);
-    if (g->pser > 0x7FFFFFFFu || g->bser > 0x7FFFFFFFu) {
-        CK(cudaMemsetAsync(g->fstamp, 0, sizeof(unsigned) * g->n, g->stream));
-        CK(cudaMemsetAsync(g->sstamp, 0, sizeof(unsigned) * g->n, g->stream));
-        g->pser = g->bser = 1;
+    // an interrupted solve may leave dedup bits set: clear them for the next one
+    if (c.abort || c.status != 0) {
+        CK(cudaMemsetAsync(g->fbits, 0, 2 * sizeof(unsigned) * g->nwords, g->stream));
+        CK(cudaMemsetAsync(g->sbits, 0, sizeof(unsigned) * g->nwords, g->stream));
+        CK(cudaStreamSynchronize(g->stream));
     }
     if (c.abort) return set_err(DS_ETIMEOUT, "solver watchdog expired (DS_TIMEOUT_S=%g)", tmo);
     if (g->trace) {
@@ -909,32 +1162,61 @@ __global__ void k_export_edges<EdgeF64>(const EdgeF64* e, long long m, int, long
 }
 
 extern "C" int ds_export_split(ds_graph* g, int which, int64_t* indptr, int64_t* col, double* val) {
+    // split_edges (sssp.py:106-150) in the caller's vertex order: the same
+    // split kernels the solver uses, run with the identity order
     if (!g) return set_err(DS_EINVAL, "null graph handle");
     if (!g->prepared) return set_err(DS_EINVAL, "graph not prepared");
     DeviceGuard guard(g->device);
+    const long long n = g->n;
     const long long m = which ? g->nH : g->nL;
-    const long long* ptr = which ? g->Hptr : g->Lptr;
-    CK(cudaMemcpyAsync(indptr, ptr, sizeof(long long) * (g->n + 1), cudaMemcpyDefault, g->stream));
+    long long *ptrL = nullptr, *ptrH = nullptr, *dcol = nullptr;
+    EdgeF64 *eL = nullptr, *eH = nullptr;
+    double* dval = nullptr;
+    int rc = DS_OK;
+    auto done = [&](int code) {
+        cudaStreamSynchronize(g->stream);
+        for (void* q : {(void*)ptrL, (void*)ptrH, (void*)dcol, (void*)eL, (void*)eH, (void*)dval})
+            if (q) cudaFree(q);
+        return code;
+    };
+#define CKE(call)                                                                             \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return done(set_err(DS_ECUDA, "CUDA error %s at %s:%d", cudaGetErrorName(e_),    \
+                                __FILE__, __LINE__));                                         \
+    } while (0)
+    CKE(cudaMalloc(&ptrL, sizeof(long long) * (n + 1)));
+    CKE(cudaMalloc(&ptrH, sizeof(long long) * (n + 1)));
+    CKE(cudaMalloc(&eL, sizeof(EdgeF64) * std::max(g->nL, 1LL)));
+    CKE(cudaMalloc(&eH, sizeof(EdgeF64) * std::max(g->nH, 1LL)));
+    CKE(cudaMemsetAsync(ptrL, 0, sizeof(long long), g->stream));
+    CKE(cudaMemsetAsync(ptrH, 0, sizeof(long long), g->stream));
+    PrepStats* st = g->pstat;
+    CKE(cudaMemsetAsync(st, 0, sizeof(PrepStats), g->stream));
+    const unsigned grid = (unsigned)(g->nsm * 16);
+    k_split_count<<<grid, 256, 0, g->stream>>>(n, g->indptr, g->w, g->delta, nullptr, g->Rpre,
+                                               g->Rbase, st);
+    CKE(cudaGetLastError());
+    if ((rc = inclusive_scan_i64(g, g->Rpre, ptrL + 1, n))) return done(rc);
+    if ((rc = inclusive_scan_i64(g, g->Rbase, ptrH + 1, n))) return done(rc);
+    k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, g->delta, 0,
+                                                          nullptr, nullptr, ptrL, ptrH, eL, eH);
+    CKE(cudaGetLastError());
+    CKE(cudaMemcpyAsync(indptr, which ? ptrH : ptrL, sizeof(long long) * (n + 1), cudaMemcpyDefault,
+                        g->stream));
     if (m > 0) {
-        long long* dcol = nullptr;
-        double* dval = nullptr;
-        CK(cudaMalloc(&dcol, sizeof(long long) * m));
-        CK(cudaMalloc(&dval, sizeof(double) * m));
-        if (g->mode == DS_MODE_FIXED32)
-            k_export_edges<uint2><<<elementwise_grid(g), 256, 0, g->stream>>>(
-                (const uint2*)(which ? g->Hedges : g->Ledges), m, g->frac, dcol, dval);
-        else
-            k_export_edges<EdgeF64><<<elementwise_grid(g), 256, 0, g->stream>>>(
-                (const EdgeF64*)(which ? g->Hedges : g->Ledges), m, 0, dcol, dval);
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(col, dcol, sizeof(long long) * m, cudaMemcpyDefault, g->stream));
-        CK(cudaMemcpyAsync(val, dval, sizeof(double) * m, cudaMemcpyDefault, g->stream));
-        CK(cudaStreamSynchronize(g->stream));
-        cudaFree(dcol);
-        cudaFree(dval);
+        CKE(cudaMalloc(&dcol, sizeof(long long) * m));
+        CKE(cudaMalloc(&dval, sizeof(double) * m));
+        k_export_edges<EdgeF64><<<elementwise_grid(g), 256, 0, g->stream>>>(which ? eH : eL, m, 0,
+                                                                            dcol, dval);
+        CKE(cudaGetLastError());
+        CKE(cudaMemcpyAsync(col, dcol, sizeof(long long) * m, cudaMemcpyDefault, g->stream));
+        CKE(cudaMemcpyAsync(val, dval, sizeof(double) * m, cudaMemcpyDefault, g->stream));
     }
-    CK(cudaStreamSynchronize(g->stream));
-    return DS_OK;
+    CKE(cudaStreamSynchronize(g->stream));
+#undef CKE
+    return done(DS_OK);
 }
 
 __global__ void k_download_w(const double* w, float* out, long long m, int* bad) {
@@ -982,6 +1264,8 @@ int ds_internal_adopt(ds_graph** out, int device, void* stream, long long n, lon
     g->col = col;
     g->w = w;
     int rc = alloc_scratch(g);
+    if (!rc) rc = compute_order(g);
+    if (!rc) rc = check_symmetric(g);
     if (rc) {
         free_all(g);
         delete g;

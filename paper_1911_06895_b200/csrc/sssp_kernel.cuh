@@ -23,18 +23,22 @@
 //    internally (same distances, test_sssp.py:365-375) and the reference's
 //    non-skip outer_iterations is recovered on the host from max(t_final).
 //
-// Work decomposition per step (all steps grid-stride over the persistent grid):
+// Work decomposition per step: every step is warp-granular -- warps of the
+// persistent grid take chunks independently and never wait on each other
+// inside a step (no __syncthreads); steps are separated by grid barriers.
 //  capture : frontier ids -> (captured d, row base, degree prefix) entries.
-//            Each CTA tile scans its degrees in shared memory and reserves
-//            its (entries, edges) ranges with ONE packed 64-bit atomicAdd, so
-//            entry ranks and edge prefixes stay consistent without a global
-//            scan; it also writes a tile->first-entry map for the relax step.
-//  relax   : edge-balanced; each CTA stages one tile's entries in shared
-//            memory, each thread maps kRelItems consecutive virtual edges to
-//            their rows, then issues all edge loads, all distance loads and
-//            finally the atomicMin pushes (three batched latency stages).
-//  Appends (next frontier, S) are staged in a per-CTA shared-memory queue and
-//  flushed with one global atomic per tile.
+//            A warp scans its chunk's degrees with shuffles and reserves its
+//            (entries, edges) ranges with ONE packed 64-bit atomicAdd, so entry
+//            ranks and edge prefixes stay consistent without a global scan; it
+//            also writes the chunk map (first entry of every 256-edge chunk).
+//  relax   : edge-balanced; a warp stages one 256-edge chunk's entries in its
+//            shared-memory slice, maps each edge to its row, then issues
+//            lane-strided (coalesced) edge loads, the distance loads and the
+//            atomicMin pushes as three batched latency stages.
+//  Dedup of the next frontier and of S uses 1 bit per vertex (L2-resident
+//  bitmaps), cleared by the step that consumes the list.  Appends are staged
+//  in the warp's shared-memory queue (ballot prefix) and flushed with one
+//  global atomic per chunk.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -121,12 +125,25 @@ struct ModeF64 {
 
 constexpr int kPackShift = 33;  // capture reservation: (entries << 33) | edges
 constexpr unsigned long long kMask33 = (1ull << kPackShift) - 1;
+constexpr int kWarps = kThreads / 32;
+constexpr int kChunk = 256;       // relax / pull: edges per warp chunk (32 lanes x 8)
+constexpr int kRelPer = kChunk / 32;
+constexpr int kListPer = 4;       // capture (list): entries per lane
+constexpr int kRangePer = 16;     // capture (range): vertices per lane
+constexpr int kQueue = 256;       // per-warp append staging (overflow spills to global)
+#ifndef DS_HEAVY_RED
+#define DS_HEAVY_RED 0
+#endif
+#ifndef DS_PRECHECK_L1
+#define DS_PRECHECK_L1 1
+#endif
+constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 
 struct StepSlot {
     unsigned long long re_packed;     // capture: reserved (entries << 33) | edges
     unsigned long long front_count;   // capture (range mode): frontier size
     unsigned long long next_min;      // capture (range mode): min D >= H
-    unsigned long long append_count;  // relax (light): next-frontier size
+    unsigned long long append_count;  // relax / pull (light): next-frontier size
     unsigned int flags;               // bit0: fixed-point overflow
     unsigned int pad;
     unsigned long long pad2[3];
@@ -142,9 +159,22 @@ struct Ctl {
     unsigned long long reached, edges_reached, max_d;
     unsigned long long phases, visited, edges_scanned, barriers, steps;
     long long last_bucket;
+    unsigned long long pulls;  // light/heavy steps run as pulls
 };
 
 constexpr int kDevOverflow = 100;  // internal status: fixed-point overflow
+
+// Pull schedule of one CSR (light or heavy) in solver order: the rows with
+// at least one edge, their offsets, the row holding the first edge of every
+// 256-edge chunk, and the rows that cross a chunk boundary (their partial
+// minima meet in `req` and are finished by the commit step).
+struct PullPlan {
+    const int* rowid;           // compacted row -> solver vertex id
+    const long long* cptr;      // compacted offsets (n_nz + 1)
+    const unsigned* chunk_row;  // nchunk + 1 entries
+    const int* span;            // compacted rows crossing a chunk boundary
+    long long n_nz, nspan, nnz;
+};
 
 template <class M>
 struct KParams {
@@ -154,7 +184,8 @@ struct KParams {
     long long source;
     double delta;
     int frac;
-    int pad;
+    int pull_enabled;
+    float pull_light, pull_heavy;  // pull when push volume > frac * nnz
     long long ceiling;
     unsigned long long timeout_ns;
     const long long* indptr;  // original CSR row offsets (for m_r)
@@ -162,52 +193,45 @@ struct KParams {
     const Edge* Ledges;
     const long long* Hptr;
     const Edge* Hedges;
+    PullPlan Lpull, Hpull;
     D* dist;
-    unsigned* fstamp;
-    unsigned* sstamp;
-    int* F0;
-    int* F1;
-    int* S;
+    D* req;              // pull partial minima (INF when idle), n_nz entries
+    unsigned* fbits[2];  // next-frontier dedup bitmaps (alternating phases)
+    unsigned* sbits;     // S membership / dedup bitmap
+    int* F[2];           // frontier lists
+    D* Fv[2];            // frontier values (lists produced by a pull)
+    int* S[2];           // S lists (alternating buckets)
     long long* Rpre;
     long long* Rbase;
     D* Rd;
-    unsigned* tile_start;
+    unsigned* chunk_start;
+    const int* perm;      // input id -> solver id (degree-sorted relabeling)
+    long long n_active;   // solver ids >= n_active have no edges at all
     Ctl* ctl;
     double* out;
     unsigned long long* trace;  // optional per-step timeline (2 words / step)
     unsigned long long trace_cap;
-    unsigned pser0, bser0;
 };
-
-constexpr int kQCap = 1024;  // per-CTA append staging (overflow spills to global)
 
 template <class D>
-struct SmemRelax {
-    long long base[kRelTile + 1];
-    D d[kRelTile + 1];
-    int rel[kRelTile + 1];
-    unsigned short row[kRelTile];  // tile-local edge -> staged entry
+struct WarpSmem {
+    long long base[kChunk + 1];
+    D d[kChunk + 1];
+    int rel[kChunk + 1];
+    unsigned short row[kChunk];
+    int q[kQueue];
+    D qv[kQueue];
 };
-
-using BlockScanU64 = cub::BlockScan<unsigned long long, kThreads>;
 
 template <class D>
 struct Smem {
-    union {
-        SmemRelax<D> rx;
-        typename BlockScanU64::TempStorage scan;
-    } u;
-    int qbuf[kQCap];
-    unsigned qcnt;
-    unsigned qn;
-    unsigned long long qbase;
-    unsigned long long red[kThreads / 32];
-    unsigned long long red2[kThreads / 32];
-    unsigned long long pc, pd;
+    WarpSmem<D> w[kWarps];
+    unsigned long long red[kWarps];
+    unsigned long long red2[kWarps];
     int ok;
 };
 
-// ---------------------------------------------------------------- block utils
+// ---------------------------------------------------------------- warp / block utils
 
 __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
 #pragma unroll
@@ -230,6 +254,14 @@ __device__ __forceinline__ unsigned long long warp_max(unsigned long long v) {
     }
     return v;
 }
+__device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
 
 // op: 0 sum, 1 min, 2 max; result valid in thread 0
 template <int OP>
@@ -241,7 +273,7 @@ __device__ __forceinline__ unsigned long long block_reduce(unsigned long long v,
     if (lane == 0) buf[w] = v;
     __syncthreads();
     if (w == 0) {
-        v = lane < kThreads / 32 ? buf[lane] : (OP == 1 ? ~0ull : 0ull);
+        v = lane < kWarps ? buf[lane] : (OP == 1 ? ~0ull : 0ull);
         v = OP == 0 ? warp_sum(v) : OP == 1 ? warp_min(v) : warp_max(v);
     }
     return v;
@@ -251,6 +283,15 @@ __device__ __forceinline__ unsigned long long evict_first_policy() {
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
+}
+
+// set bit v; true iff it was clear (first claim this phase / bucket)
+__device__ __forceinline__ bool claim_bit(unsigned* bits, unsigned v) {
+    const unsigned m = 1u << (v & 31);
+    return (atomicOr(bits + (v >> 5), m) & m) == 0;
+}
+__device__ __forceinline__ bool test_bit(const unsigned* bits, unsigned v) {
+    return (__ldcg(bits + (v >> 5)) >> (v & 31)) & 1u;
 }
 
 // Grid-wide barrier over a co-resident (cooperative) grid.  Returns false if
@@ -292,38 +333,48 @@ __device__ __forceinline__ bool grid_sync(Ctl* c, unsigned& gen, unsigned long l
     return sm.ok != 0;
 }
 
-// Stage v in the CTA's shared-memory queue (warp-aggregated); spill straight
+// Warp-uniform append: every lane calls it; lanes with `want` land in the
+// warp's queue at ballot-prefix positions (optionally with a value).  Spills
 // to the global list when the queue is full.
-template <class S>
-__device__ __forceinline__ void q_push(S& sm, int* list, unsigned long long* counter, int v) {
-    cg::coalesced_group g = cg::coalesced_threads();
-    unsigned pos = 0;
-    if (g.thread_rank() == 0) pos = atomicAdd(&sm.qcnt, (unsigned)g.size());
-    pos = g.shfl(pos, 0) + g.thread_rank();
-    if (pos < (unsigned)kQCap) {
-        sm.qbuf[pos] = v;
+template <class D, bool VAL>
+__device__ __forceinline__ void wq_push(int* q, D* qv, unsigned& qn, bool want, int v, D val,
+                                        int lane, int* list, D* vlist,
+                                        unsigned long long* counter) {
+    const unsigned m = __ballot_sync(0xffffffffu, want);
+    if (!m) return;
+    const unsigned cnt = __popc(m);
+    const unsigned below = __popc(m & ((1u << lane) - 1u));
+    if (qn + cnt <= (unsigned)kQueue) {
+        if (want) {
+            q[qn + below] = v;
+            if (VAL) qv[qn + below] = val;
+        }
+        qn += cnt;
     } else {
-        cg::coalesced_group h = cg::coalesced_threads();
         unsigned long long b = 0;
-        if (h.thread_rank() == 0) b = atomicAdd(counter, (unsigned long long)h.size());
-        b = h.shfl(b, 0);
-        list[b + h.thread_rank()] = v;
+        if (lane == 0) b = atomicAdd(counter, (unsigned long long)cnt);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (want) {
+            list[b + below] = v;
+            if (VAL) vlist[b + below] = val;
+        }
     }
 }
 
-// Reserve global space for the staged queue (thread 0); call between two
-// __syncthreads, then q_copy after the second.
-template <class S>
-__device__ __forceinline__ void q_reserve(S& sm, unsigned long long* counter) {
-    const unsigned c = sm.qcnt < (unsigned)kQCap ? sm.qcnt : (unsigned)kQCap;
-    sm.qn = c;
-    sm.qbase = c ? atomicAdd(counter, (unsigned long long)c) : 0ull;
-    sm.qcnt = 0;
-}
-template <class S>
-__device__ __forceinline__ void q_copy(S& sm, int* list) {
-    const unsigned c = sm.qn;
-    for (unsigned i = threadIdx.x; i < c; i += kThreads) list[sm.qbase + i] = sm.qbuf[i];
+template <class D, bool VAL>
+__device__ __forceinline__ void wq_flush(int* q, D* qv, unsigned& qn, int lane, int* list,
+                                         D* vlist, unsigned long long* counter) {
+    if (!qn) return;
+    __syncwarp();
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(counter, (unsigned long long)qn);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    for (unsigned i = lane; i < qn; i += 32) {
+        list[b + i] = q[i];
+        if (VAL) vlist[b + i] = qv[i];
+    }
+    __syncwarp();
+    qn = 0;
 }
 
 // ---------------------------------------------------------------- capture step
@@ -331,209 +382,487 @@ __device__ __forceinline__ void q_copy(S& sm, int* list) {
 // Input: a frontier given as an id list (LIST) or as "all vertices whose
 // distance lies in [L, H)" (RANGE: compute_bucket, sssp.py:153-158).
 // Output: compacted entries (captured d, row base, degree prefix) of the
-// frontier vertices with at least one edge in `ptr`'s CSR, the relax tile
+// frontier vertices with at least one edge in `ptr`'s CSR, the relax chunk
 // map, and the slot totals.  APPEND_S adds every frontier vertex to S
-// (S = S + t_Bi, sssp.py:191; dedup by the bucket stamp).
+// (S = S + t_Bi, sssp.py:191; dedup by the S bitmap).
 
-template <class M, bool RANGE, bool APPEND_S>
-__device__ void capture_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
-                             const int* list, unsigned long long count, typename M::D L,
-                             typename M::D H, const long long* ptr, unsigned bser,
-                             unsigned long long* s_counter) {
-    using D = typename M::D;
-    const unsigned long long total = RANGE ? (unsigned long long)p.n : count;
-    const unsigned long long ntiles = (total + kCapTile - 1) / kCapTile;
-    unsigned long long local_fc = 0;
-    unsigned long long local_min = ~0ull;
-
-    for (unsigned long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        __syncthreads();  // shared queue / scan storage reuse across tiles
-        const unsigned long long base = tile * kCapTile + (unsigned long long)threadIdx.x * kCapItems;
-        int vtx[kCapItems];
-        D dv[kCapItems];
-        bool in[kCapItems];
+template <class M, int PER>
+__device__ __forceinline__ void capture_emit(const KParams<M>& p, StepSlot* slot, int lane,
+                                             const typename M::D (&dv)[PER],
+                                             const long long (&off)[PER], const long long (&deg)[PER]) {
+    unsigned long long packed = 0;  // (count << 48) | degree within the warp chunk
 #pragma unroll
-        for (int j = 0; j < kCapItems; ++j) {
-            const unsigned long long idx = base + j;
-            in[j] = idx < total;
-            vtx[j] = in[j] ? (RANGE ? (int)idx : ldcg(list + idx)) : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < kCapItems; ++j) dv[j] = in[j] ? __ldcg(p.dist + vtx[j]) : M::INF;
-        long long off[kCapItems];
-        long long deg[kCapItems];
-        unsigned long long packed = 0;  // (count << 48) | degree within the tile
-#pragma unroll
-        for (int j = 0; j < kCapItems; ++j) {
-            if (RANGE && in[j]) {
-                const D d = dv[j];
-                if (d >= H && d != M::INF && (unsigned long long)d < local_min)
-                    local_min = (unsigned long long)d;
-                in[j] = (d >= L) && (d < H);
-            }
-            off[j] = in[j] ? __ldg(ptr + vtx[j]) : 0;
-            deg[j] = in[j] ? __ldg(ptr + vtx[j] + 1) : 0;
-        }
-#pragma unroll
-        for (int j = 0; j < kCapItems; ++j) {
-            if (in[j]) {
-                ++local_fc;
-                if (APPEND_S) {
-                    if (atomicExch(p.sstamp + vtx[j], bser) != bser) q_push(sm, p.S, s_counter, vtx[j]);
-                }
-                deg[j] -= off[j];
-                if (deg[j] > 0) packed += (1ull << 48) + (unsigned long long)deg[j];
-            } else {
-                deg[j] = 0;
-            }
-        }
-        unsigned long long excl, agg;
-        BlockScanU64(sm.u.scan).ExclusiveSum(packed, excl, agg);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            // one packed reservation keeps entry ranks and edge prefixes in
-            // the same order across tiles
-            if (agg) {
-                const unsigned long long want = ((agg >> 48) << kPackShift) | (agg & kMask48);
-                const unsigned long long r = atomicAdd(&slot->re_packed, want);
-                sm.pc = r >> kPackShift;
-                sm.pd = r & kMask33;
-            }
-            if (APPEND_S) q_reserve(sm, s_counter);
-        }
-        __syncthreads();
-        if (APPEND_S) q_copy(sm, p.S);
-        if (agg) {
-            unsigned long long rank = sm.pc + (excl >> 48);
-            unsigned long long pre = sm.pd + (excl & kMask48);
-#pragma unroll
-            for (int j = 0; j < kCapItems; ++j) {
-                if (deg[j] > 0) {
-                    p.Rpre[rank] = (long long)pre;
-                    p.Rbase[rank] = off[j] - (long long)pre;
-                    p.Rd[rank] = dv[j];
-                    const unsigned long long t0 = (pre + kRelTile - 1) / kRelTile;
-                    const unsigned long long t1 = (pre + (unsigned long long)deg[j] - 1) / kRelTile;
-                    for (unsigned long long t = t0; t <= t1; ++t) p.tile_start[t] = (unsigned)rank;
-                    ++rank;
-                    pre += (unsigned long long)deg[j];
-                }
-            }
-        }
+    for (int j = 0; j < PER; ++j)
+        if (deg[j] > 0) packed += (1ull << 48) + (unsigned long long)deg[j];
+    const unsigned long long incl = warp_incl_scan(packed, lane);
+    const unsigned long long tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (!tot) return;
+    unsigned long long r = 0;
+    if (lane == 31) {
+        // one packed reservation keeps entry ranks and edge prefixes in the
+        // same order across warps
+        const unsigned long long want = ((tot >> 48) << kPackShift) | (tot & kMask48);
+        r = atomicAdd(&slot->re_packed, want);
     }
-    if (RANGE) {
-        const unsigned long long fc = block_reduce<0>(local_fc, sm.red);
-        const unsigned long long mn = block_reduce<1>(local_min, sm.red2);
-        if (threadIdx.x == 0) {
-            if (fc) atomicAdd(&slot->front_count, fc);
-            if (mn != ~0ull) atomicMin(&slot->next_min, mn);
+    r = __shfl_sync(0xffffffffu, r, 31);
+    const unsigned long long excl = incl - packed;
+    unsigned long long rank = (r >> kPackShift) + (excl >> 48);
+    unsigned long long pre = (r & kMask33) + (excl & kMask48);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        if (deg[j] > 0) {
+            p.Rpre[rank] = (long long)pre;
+            p.Rbase[rank] = off[j] - (long long)pre;
+            p.Rd[rank] = dv[j];
+            const unsigned long long t0 = (pre + kChunk - 1) / kChunk;
+            const unsigned long long t1 = (pre + (unsigned long long)deg[j] - 1) / kChunk;
+            for (unsigned long long t = t0; t <= t1; ++t) p.chunk_start[t] = (unsigned)rank;
+            ++rank;
+            pre += (unsigned long long)deg[j];
         }
     }
 }
 
-// ---------------------------------------------------------------- relax step
+template <class D>
+__device__ __forceinline__ void load_run(const D* p, D (&out)[kRangePer]);
+template <>
+__device__ __forceinline__ void load_run<unsigned>(const unsigned* p, unsigned (&out)[kRangePer]) {
+#pragma unroll
+    for (int i = 0; i < kRangePer / 4; ++i) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(p) + i);
+        out[4 * i] = q.x;
+        out[4 * i + 1] = q.y;
+        out[4 * i + 2] = q.z;
+        out[4 * i + 3] = q.w;
+    }
+}
+template <>
+__device__ __forceinline__ void load_run<unsigned long long>(const unsigned long long* p,
+                                                             unsigned long long (&out)[kRangePer]) {
+#pragma unroll
+    for (int i = 0; i < kRangePer / 2; ++i) {
+        const ulonglong2 q = __ldcg(reinterpret_cast<const ulonglong2*>(p) + i);
+        out[2 * i] = q.x;
+        out[2 * i + 1] = q.y;
+    }
+}
+
+// RANGE capture: bucket extraction by a dense scan of the distance array.
+// Also retires the previous bucket's S bits (atomicAnd: disjoint from the
+// new bucket's S, which only holds vertices with values >= the old hi).
+template <class M>
+__device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
+                              typename M::D L, typename M::D H, int* S, unsigned long long* s_counter,
+                              unsigned long long n_scan, const int* old_S, unsigned long long old_count) {
+    using D = typename M::D;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem<D>& ws = sm.w[wib];
+    unsigned qn = 0;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    for (unsigned long long i = gw * 32 + lane; i < old_count; i += nw * 32) {
+        const unsigned v = (unsigned)ldcg(old_S + i);
+        atomicAnd(p.sbits + (v >> 5), ~(1u << (v & 31)));
+    }
+    const unsigned long long n = n_scan;
+    const unsigned long long per_chunk = 32ull * kRangePer;
+    const unsigned long long nchunk = (n + per_chunk - 1) / per_chunk;
+    unsigned long long local_fc = 0, local_min = ~0ull;
+    for (unsigned long long c = gw; c < nchunk; c += nw) {
+        const unsigned long long v0 = c * per_chunk + (unsigned long long)lane * kRangePer;
+        D dv[kRangePer];
+        if (v0 + kRangePer <= n) {
+            load_run<D>(p.dist + v0, dv);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kRangePer; ++j) dv[j] = v0 + j < n ? __ldcg(p.dist + v0 + j) : M::INF;
+        }
+        unsigned hits = 0;
+#pragma unroll
+        for (int j = 0; j < kRangePer; ++j) {
+            const D d = dv[j];
+            if (d >= H && d != M::INF && (unsigned long long)d < local_min) local_min = (unsigned long long)d;
+            if (d >= L && d < H) hits |= 1u << j;
+        }
+        if (!__any_sync(0xffffffffu, hits != 0)) continue;
+        local_fc += __popc(hits);
+        // in-window vertices of this chunk, kListPer per lane per round
+        D cd[kListPer];
+        long long off[kListPer], deg[kListPer];
+        unsigned rem = hits;
+        while (__any_sync(0xffffffffu, rem != 0)) {
+            int vtx[kListPer];
+#pragma unroll
+            for (int j = 0; j < kListPer; ++j) {
+                deg[j] = 0;
+                off[j] = 0;
+                vtx[j] = -1;
+                cd[j] = 0;
+                if (rem) {
+                    const int b = __ffs(rem) - 1;
+                    rem &= rem - 1;
+                    vtx[j] = (int)(v0 + b);
+                    cd[j] = dv[b];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kListPer; ++j) {
+                const bool in = vtx[j] >= 0;
+                if (in) {
+                    off[j] = __ldg(p.Lptr + vtx[j]);
+                    deg[j] = __ldg(p.Lptr + vtx[j] + 1) - off[j];
+                }
+                const bool news = in && claim_bit(p.sbits, (unsigned)vtx[j]);
+                wq_push<D, false>(ws.q, ws.qv, qn, news, vtx[j], (D)0, lane, S, nullptr, s_counter);
+            }
+            capture_emit<M, kListPer>(p, slot, lane, cd, off, deg);
+        }
+        wq_flush<D, false>(ws.q, ws.qv, qn, lane, S, nullptr, s_counter);
+    }
+    const unsigned long long fc = block_reduce<0>(local_fc, sm.red);
+    const unsigned long long mn = block_reduce<1>(local_min, sm.red2);
+    if (threadIdx.x == 0) {
+        if (fc) atomicAdd(&slot->front_count, fc);
+        if (mn != ~0ull) atomicMin(&slot->next_min, mn);
+    }
+}
+
+// LIST capture: a frontier / S list.  Snapshots d after the barrier that
+// ended the previous phase (VALS: the list carries values produced by a pull
+// and this step commits them to t first), looks up degrees in `ptr`, clears
+// the next-frontier dedup bits for their next use, optionally adds to S.
+template <class M, bool APPEND_S, bool VALS>
+__device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
+                             const int* list, const typename M::D* vals, unsigned long long count,
+                             const long long* ptr, unsigned* clear_bits, int* S,
+                             unsigned long long* s_counter) {
+    using D = typename M::D;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem<D>& ws = sm.w[wib];
+    unsigned qn = 0;
+    const unsigned long long per_chunk = 32ull * kListPer;
+    const unsigned long long nchunk = (count + per_chunk - 1) / per_chunk;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    for (unsigned long long c = gw; c < nchunk; c += nw) {
+        int vtx[kListPer];
+        bool in[kListPer];
+        D dv[kListPer];
+#pragma unroll
+        for (int j = 0; j < kListPer; ++j) {
+            const unsigned long long idx = c * per_chunk + lane + 32ull * j;
+            in[j] = idx < count;
+            vtx[j] = in[j] ? ldcg(list + idx) : 0;
+            if (VALS) dv[j] = in[j] ? __ldcg(vals + idx) : (D)0;
+        }
+        long long off[kListPer], deg[kListPer];
+#pragma unroll
+        for (int j = 0; j < kListPer; ++j) {
+            if (VALS) {
+                if (in[j]) p.dist[vtx[j]] = dv[j];
+            } else {
+                dv[j] = in[j] ? __ldcg(p.dist + vtx[j]) : (D)0;
+            }
+            off[j] = in[j] ? __ldg(ptr + vtx[j]) : 0;
+            deg[j] = in[j] ? __ldg(ptr + vtx[j] + 1) - off[j] : 0;
+            if (in[j] && clear_bits) clear_bits[(unsigned)vtx[j] >> 5] = 0u;
+        }
+        if (APPEND_S) {
+#pragma unroll
+            for (int j = 0; j < kListPer; ++j) {
+                const bool news = in[j] && claim_bit(p.sbits, (unsigned)vtx[j]);
+                wq_push<D, false>(ws.q, ws.qv, qn, news, vtx[j], (D)0, lane, S, nullptr, s_counter);
+            }
+            wq_flush<D, false>(ws.q, ws.qv, qn, lane, S, nullptr, s_counter);
+        }
+        capture_emit<M, kListPer>(p, slot, lane, dv, off, deg);
+    }
+}
+
+// ---------------------------------------------------------------- relax step (push)
 //
 // Edge-balanced push over the entries of the last capture.  LIGHT: successful
 // improvements that land inside the window join the next frontier once
-// (fstamp dedup); HEAVY: min-merge only (results land beyond the window).
+// (bitmap dedup); HEAVY: min-merge only (results land beyond the window).
 
 template <class M, bool LIGHT>
 __device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                            unsigned long long E, unsigned long long Rc,
                            const typename M::Edge* edges, typename M::D H, int* out_list,
-                           unsigned pser) {
+                           unsigned* fbits) {
     using D = typename M::D;
     using Edge = typename M::Edge;
-    const unsigned long long ntile = (E + kRelTile - 1) / kRelTile;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem<D>& ws = sm.w[wib];
+    unsigned qn = 0;
+    const unsigned long long nchunk = (E + kChunk - 1) / kChunk;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
     const unsigned long long pol = evict_first_policy();
     bool overflow = false;
-    for (unsigned long long t = blockIdx.x; t < ntile; t += gridDim.x) {
-        const unsigned long long r0 = ldcg(p.tile_start + t);
-        const unsigned long long r1 = (t + 1 < ntile) ? ldcg(p.tile_start + t + 1) : Rc - 1;
+    for (unsigned long long c = gw; c < nchunk; c += nw) {
+        const unsigned long long r0 = ldcg(p.chunk_start + c);
+        const unsigned long long r1 = (c + 1 < nchunk) ? ldcg(p.chunk_start + c + 1) : Rc - 1;
         const int ne = (int)(r1 - r0 + 1);
-        const long long tb = (long long)(t * kRelTile);
-        for (int k = threadIdx.x; k < ne; k += kThreads) {
+        const long long cb = (long long)(c * kChunk);
+        for (int k = lane; k < ne; k += 32) {
             const unsigned long long r = r0 + k;
-            const long long rel = ldcg(p.Rpre + r) - tb;
-            sm.u.rx.rel[k] = rel < 0 ? 0 : (int)rel;
-            sm.u.rx.base[k] = ldcg(p.Rbase + r);
-            sm.u.rx.d[k] = __ldcg(p.Rd + r);
+            const long long rel = ldcg(p.Rpre + r) - cb;
+            ws.rel[k] = rel < 0 ? 0 : (int)rel;
+            ws.base[k] = ldcg(p.Rbase + r);
+            ws.d[k] = __ldcg(p.Rd + r);
         }
-        __syncthreads();
-        // row map: thread t resolves the staged entry of tile edges
-        // [8t, 8t+8) with one binary search and a short walk
-        {
-            const int rel0 = threadIdx.x * kRelItems;
+        __syncwarp();
+        {   // row map: lane resolves the entry of chunk edges [8 lane, 8 lane + 8)
+            const int rel0 = lane * kRelPer;
             int lo = 0, hi = ne;
             while (hi - lo > 1) {
                 const int mid = (lo + hi) >> 1;
-                if (sm.u.rx.rel[mid] <= rel0) lo = mid;
+                if (ws.rel[mid] <= rel0) lo = mid;
                 else hi = mid;
             }
             int k = lo;
 #pragma unroll
-            for (int j = 0; j < kRelItems; ++j) {
-                while (k + 1 < ne && sm.u.rx.rel[k + 1] <= rel0 + j) ++k;
-                sm.u.rx.row[rel0 + j] = (unsigned short)k;
+            for (int j = 0; j < kRelPer; ++j) {
+                while (k + 1 < ne && ws.rel[k + 1] <= rel0 + j) ++k;
+                ws.row[rel0 + j] = (unsigned short)k;
             }
         }
-        __syncthreads();
-        // edges are taken lane-strided (edge = tb + tid + 256 j) so every warp
-        // load instruction reads 32 consecutive (col, w) pairs
-        const long long left = (long long)E - tb - threadIdx.x;  // > 256 j  <=>  edge j exists
-        if (left > 0) {
-            int kk[kRelItems];
-            Edge ed[kRelItems];
+        __syncwarp();
+        const long long left = (long long)E - cb - lane;  // edge j exists iff 32 j < left
+        int kk[kRelPer];
+        Edge ed[kRelPer];
 #pragma unroll
-            for (int j = 0; j < kRelItems; ++j) {
-                const int r = threadIdx.x + j * kThreads;
-                kk[j] = sm.u.rx.row[r];
-                if (j * kThreads < left) ed[j] = M::load(edges + (sm.u.rx.base[kk[j]] + tb + r), pol);
-            }
-            // stage 2: candidate distances and current values
-            D nd[kRelItems], cur[kRelItems];
+        for (int j = 0; j < kRelPer; ++j) {
+            const int r = lane + 32 * j;
+            kk[j] = ws.row[r];
+            if (32 * j < left) ed[j] = M::load(edges + (ws.base[kk[j]] + cb + r), pol);
+        }
+        D nd[kRelPer], cur[kRelPer];
 #pragma unroll
-            for (int j = 0; j < kRelItems; ++j) {
-                cur[j] = (D)0;
-                if (j * kThreads < left) {
-                    if (M::add(sm.u.rx.d[kk[j]], ed[j], nd[j])) {
-                        cur[j] = __ldcg(p.dist + M::col(ed[j]));
-                    } else {
-                        overflow = true;
-                    }
-                }
-            }
-            // stage 3: pushes
-#pragma unroll
-            for (int j = 0; j < kRelItems; ++j) {
-                if (j * kThreads < left && nd[j] < cur[j]) {
-                    const unsigned v = M::col(ed[j]);
-                    if (LIGHT) {
-                        const D old = atomicMin(p.dist + v, nd[j]);
-                        if (nd[j] < old && nd[j] < H) {
-                            if (atomicExch(p.fstamp + v, pser) != pser)
-                                q_push(sm, out_list, &slot->append_count, (int)v);
-                        }
-                    } else {
-                        atomicMin(p.dist + v, nd[j]);
-                    }
+        for (int j = 0; j < kRelPer; ++j) {
+            cur[j] = (D)0;
+            if (32 * j < left) {
+                if (M::add(ws.d[kk[j]], ed[j], nd[j])) {
+                    // a stale (L1) value is >= the current one: it can only
+                    // cause a redundant atomic, never a missed improvement
+                    cur[j] = (LIGHT || !kHeavyRed)
+                                 ? (DS_PRECHECK_L1 ? p.dist[M::col(ed[j])] : __ldcg(p.dist + M::col(ed[j])))
+                                 : M::INF;
+                } else {
+                    overflow = true;
                 }
             }
         }
-        __syncthreads();
-        if (LIGHT) {
-            if (threadIdx.x == 0) q_reserve(sm, &slot->append_count);
-            __syncthreads();
-            q_copy(sm, out_list);
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j) {
+            const bool go = 32 * j < left && nd[j] < cur[j];
+            const unsigned v = go ? M::col(ed[j]) : 0u;
+            if (LIGHT) {
+                bool want = false;
+                if (go) {
+                    const D old = atomicMin(p.dist + v, nd[j]);
+                    want = nd[j] < old && nd[j] < H && claim_bit(fbits, v);
+                }
+                wq_push<D, false>(ws.q, ws.qv, qn, want, (int)v, (D)0, lane, out_list, nullptr,
+                                  &slot->append_count);
+            } else if (go) {
+                atomicMin(p.dist + v, nd[j]);
+            }
+        }
+        if (LIGHT) wq_flush<D, false>(ws.q, ws.qv, qn, lane, out_list, nullptr, &slot->append_count);
+        __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, 1u);
+}
+
+// ---------------------------------------------------------------- pull step
+//
+// The reference's own formulation of a relaxation -- a (min,+) product
+// gathered through the transposed matrix (fused_masked_relax,
+// fused.py:127-161; vxm_min_plus, ops.py:238-271) -- used when the frontier
+// touches a large share of the edges.  Needs A^T = A (symmetric graphs).
+//  LIGHT: an edge u->v contributes iff t[u] lies in the bucket window.  That
+//    gates a superset of the frontier, but every in-window vertex outside the
+//    frontier already pushed its current value, so the improving minima are
+//    exactly the frontier's.  In-window improvements are NOT written to t
+//    (they would change the gate mid-phase): they become the next frontier
+//    with their values and the next capture commits them.  Improvements
+//    beyond the window are written directly (they never pass the gate).
+//  HEAVY: u contributes iff u is in S (bitmap); S values are final.
+// Rows are reduced per 256-edge chunk in shared memory; rows crossing a
+// chunk boundary combine partial minima in `req` for the commit step.
+
+template <class M, bool LIGHT>
+__device__ __forceinline__ void pull_row_commit(const KParams<M>& p, typename M::D rmin, int rr,
+                                                typename M::D H, bool& want, typename M::D& val) {
+    const typename M::D cur = __ldcg(p.dist + rr);
+    if (rmin < cur) {
+        if (LIGHT && rmin < H) {
+            want = true;
+            val = rmin;
+        } else {
+            p.dist[rr] = rmin;
         }
     }
-    if (overflow) atomicOr(&slot->flags, 1u);
+}
+
+template <class M, bool LIGHT>
+__device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
+                          const PullPlan& pl, const typename M::Edge* edges, typename M::D L,
+                          typename M::D H, int* out_list, typename M::D* out_vals) {
+    using D = typename M::D;
+    using Edge = typename M::Edge;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem<D>& ws = sm.w[wib];
+    unsigned qn = 0;
+    const unsigned long long nchunk = ((unsigned long long)pl.nnz + kChunk - 1) / kChunk;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    const unsigned long long pol = evict_first_policy();
+    bool overflow = false;
+    for (unsigned long long c = gw; c < nchunk; c += nw) {
+        const long long e0 = (long long)(c * kChunk);
+        const long long e1 = e0 + kChunk < pl.nnz ? e0 + kChunk : pl.nnz;
+        const int k0 = (int)__ldg(pl.chunk_row + c);
+        const int k1 = (int)__ldg(pl.chunk_row + c + 1);
+        const int ne = k1 - k0 + 1;
+        for (int i = lane; i < ne; i += 32) {
+            ws.rel[i] = (int)(__ldg(pl.cptr + k0 + i) - e0);   // may be < 0 (row began earlier)
+            ws.base[i] = __ldg(pl.cptr + k0 + i + 1);           // row end
+            ws.d[i] = M::INF;                                   // row minimum
+        }
+        __syncwarp();
+        {   // row map
+            const int rel0 = lane * kRelPer;
+            int lo = 0, hi = ne;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (ws.rel[mid] <= rel0) lo = mid;
+                else hi = mid;
+            }
+            int k = lo;
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                while (k + 1 < ne && ws.rel[k + 1] <= rel0 + j) ++k;
+                ws.row[rel0 + j] = (unsigned short)k;
+            }
+        }
+        __syncwarp();
+        const long long left = e1 - e0 - lane;
+        Edge ed[kRelPer];
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j)
+            if (32 * j < left) ed[j] = M::load(edges + (e0 + lane + 32 * j), pol);
+        // Heavy gate reads go through L1: within a heavy pull the S bits and S
+        // values are frozen, and L1 is invalidated at every grid barrier
+        // (gpu-scope fence -> CCTL.IVALL).
+        D du[kRelPer];
+        bool gate[kRelPer];
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j) {
+            gate[j] = false;
+            if (32 * j < left) {
+                const unsigned u = M::col(ed[j]);
+                if (LIGHT) {
+                    du[j] = __ldcg(p.dist + u);
+                    gate[j] = du[j] >= L && du[j] < H;
+                } else {
+                    gate[j] = (p.sbits[u >> 5] >> (u & 31)) & 1u;
+                    if (gate[j]) du[j] = p.dist[u];
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j) {
+            // segmented min over the lanes of this 32-edge window (rows are
+            // contiguous runs), then one shared atomic per run
+            D val = M::INF;
+            if (gate[j]) {
+                D nd;
+                if (M::add(du[j], ed[j], nd)) val = nd;
+                else overflow = true;
+            }
+            const int k = ws.row[lane + 32 * j];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const D ov = __shfl_up_sync(0xffffffffu, val, o);
+                const int ok = __shfl_up_sync(0xffffffffu, k, o);
+                if (lane >= o && ok == k && ov < val) val = ov;
+            }
+            const int kn = __shfl_down_sync(0xffffffffu, k, 1);
+            if ((lane == 31 || kn != k) && val != M::INF) atomicMin(&ws.d[k], val);
+        }
+        __syncwarp();
+        for (int b = 0; b < ne; b += 32) {
+            const int i = b + lane;
+            bool want = false;
+            D val = (D)0;
+            int rr = 0;
+            if (i < ne) {
+                const D rmin = ws.d[i];
+                if (rmin != M::INF) {
+                    rr = __ldg(pl.rowid + k0 + i);
+                    if (ws.rel[i] >= 0 && ws.base[i] <= e1) {
+                        pull_row_commit<M, LIGHT>(p, rmin, rr, H, want, val);
+                    } else {
+                        atomicMin(p.req + (k0 + i), rmin);  // row continues in other chunks
+                    }
+                }
+            }
+            if (LIGHT)
+                wq_push<D, true>(ws.q, ws.qv, qn, want, rr, val, lane, out_list, out_vals,
+                                 &slot->append_count);
+        }
+        if (LIGHT) wq_flush<D, true>(ws.q, ws.qv, qn, lane, out_list, out_vals, &slot->append_count);
+        __syncwarp();
+    }
+    if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, 1u);
+}
+
+// Finish rows that crossed chunk boundaries (after the pull step's barrier).
+template <class M, bool LIGHT>
+__device__ void commit_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
+                            const PullPlan& pl, typename M::D H, int* out_list,
+                            typename M::D* out_vals) {
+    using D = typename M::D;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem<D>& ws = sm.w[wib];
+    unsigned qn = 0;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    for (unsigned long long b = gw * 32; b < (unsigned long long)pl.nspan; b += nw * 32) {
+        const unsigned long long i = b + lane;
+        bool want = false;
+        D val = (D)0;
+        int rr = 0;
+        if (i < (unsigned long long)pl.nspan) {
+            const int k = __ldg(pl.span + i);
+            const D rmin = __ldcg(p.req + k);
+            if (rmin != M::INF) {
+                p.req[k] = M::INF;
+                rr = __ldg(pl.rowid + k);
+                const D cur = __ldcg(p.dist + rr);
+                if (rmin < cur) {
+                    p.dist[rr] = rmin;
+                    if (LIGHT && rmin < H) {
+                        want = true;
+                        val = rmin;
+                    }
+                }
+            }
+        }
+        if (LIGHT)
+            wq_push<D, true>(ws.q, ws.qv, qn, want, rr, val, lane, out_list, out_vals,
+                             &slot->append_count);
+    }
+    if (LIGHT) wq_flush<D, true>(ws.q, ws.qv, qn, lane, out_list, out_vals, &slot->append_count);
 }
 
 // ---------------------------------------------------------------- the solver
 
 template <class M>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     sssp_persistent_kernel(const KParams<M> p) {
     using D = typename M::D;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -541,16 +870,17 @@ __global__ void __launch_bounds__(kThreads, 3)
     Ctl* const c = p.ctl;
     unsigned gen = 0;
     unsigned long long deadline = 0;
-    if (threadIdx.x == 0) {
-        deadline = globaltimer_ns() + p.timeout_ns;
-        sm.qcnt = 0;
-    }
+    if (threadIdx.x == 0) deadline = globaltimer_ns() + p.timeout_ns;
 
-    // ---- init: t = {source: 0} (sssp.py:276), all else +inf
+    // ---- init: t = {source: 0} (sssp.py:276), all else +inf.  Only solver
+    // ids below n_scan can ever be reached (the source may be an isolated
+    // vertex outside the active prefix).
+    const long long src = __ldg(p.perm + p.source);
+    const long long n_scan = p.n_active > src + 1 ? p.n_active : src + 1;
     {
         const long long stride = (long long)gridDim.x * kThreads;
-        for (long long v = (long long)blockIdx.x * kThreads + threadIdx.x; v < p.n; v += stride)
-            p.dist[v] = (v == p.source) ? (D)0 : M::INF;
+        for (long long v = (long long)blockIdx.x * kThreads + threadIdx.x; v < n_scan; v += stride)
+            p.dist[v] = (v == src) ? (D)0 : M::INF;
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             for (int k = 0; k < 3; ++k) {
                 StepSlot* s = &c->slot[k];
@@ -565,10 +895,9 @@ __global__ void __launch_bounds__(kThreads, 3)
     if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) c->last_bucket = (long long)globaltimer_ns();
 
     unsigned long long st = 0;  // step counter (identical on every CTA)
-    unsigned long long nbar = 1, escanned = 0;
+    unsigned long long nbar = 1, escanned = 0, npull = 0;
     long long idx = 0;  // bucket index
     unsigned long long phases = 0, visited = 0;
-    unsigned pser = p.pser0, bser = p.bser0;
     int pp = 0;
     int status = 0;
 
@@ -589,6 +918,12 @@ __global__ void __launch_bounds__(kThreads, 3)
         return ok;
     };
     auto prev = [&]() -> StepSlot* { return &c->slot[(st + 2) % 3]; };
+    unsigned bpar = 0;                  // S list / counter parity (flips per visited bucket)
+    unsigned long long old_scount = 0;  // previous bucket's S, retired by the next scan
+    const unsigned long long pullL =
+        p.pull_enabled ? (unsigned long long)(p.pull_light * (float)p.Lpull.nnz) : ~0ull;
+    const unsigned long long pullH =
+        p.pull_enabled ? (unsigned long long)(p.pull_heavy * (float)p.Hpull.nnz) : ~0ull;
 
     for (;;) {
         const double lo = (double)idx * p.delta;
@@ -597,10 +932,11 @@ __global__ void __launch_bounds__(kThreads, 3)
         M::window(lo, hi, p.frac, L, H);
 
         // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
-        if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[(bser & 1) ^ 1] = 0;
-        capture_step<M, true, true>(p, sm, &c->slot[st % 3], nullptr, 0, L, H, p.Lptr, bser,
-                                    &c->s_count[bser & 1]);
-        if (!end_step(0, (unsigned long long)p.n)) return;
+        if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[bpar ^ 1] = 0;
+        capture_range<M>(p, sm, &c->slot[st % 3], L, H, p.S[bpar], &c->s_count[bpar],
+                         (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount);
+        old_scount = 0;
+        if (!end_step(0, (unsigned long long)n_scan)) return;
         const unsigned long long fc = ldcg(&prev()->front_count);
         unsigned long long re = ldcg(&prev()->re_packed);
         if (fc == 0) {
@@ -619,11 +955,28 @@ __global__ void __launch_bounds__(kThreads, 3)
                 break;
             }
             unsigned long long nf = 0;
+            bool vals = false;
             const unsigned long long E = re & kMask33;
-            if (E > 0) {
+            unsigned* fb = p.fbits[phases & 1];
+            if (E > pullL) {
+                escanned += (unsigned long long)p.Lpull.nnz;
+                ++npull;
+                const unsigned sl = (unsigned)(st % 3);
+                pull_step<M, true>(p, sm, &c->slot[sl], p.Lpull, p.Ledges, L, H, p.F[pp], p.Fv[pp]);
+                if (!end_step(5, (unsigned long long)p.Lpull.nnz)) return;
+                const bool ovf = ldcg(&prev()->flags) & 1u;
+                commit_step<M, true>(p, sm, &c->slot[sl], p.Lpull, H, p.F[pp], p.Fv[pp]);
+                if (!end_step(6, (unsigned long long)p.Lpull.nspan)) return;
+                if (ovf) {
+                    status = kDevOverflow;
+                    break;
+                }
+                nf = ldcg(&c->slot[sl].append_count);
+                vals = true;
+            } else if (E > 0) {
                 escanned += E;
                 relax_step<M, true>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Ledges, H,
-                                    pp ? p.F1 : p.F0, pser);
+                                    p.F[pp], fb);
                 if (!end_step(1, E)) return;
                 if (ldcg(&prev()->flags) & 1u) {
                     status = kDevOverflow;
@@ -631,10 +984,13 @@ __global__ void __launch_bounds__(kThreads, 3)
                 }
                 nf = ldcg(&prev()->append_count);
             }
-            ++pser;
             if (nf == 0) break;
-            capture_step<M, false, true>(p, sm, &c->slot[st % 3], pp ? p.F1 : p.F0, nf, L, H,
-                                         p.Lptr, bser, &c->s_count[bser & 1]);
+            if (vals)
+                capture_list<M, true, true>(p, sm, &c->slot[st % 3], p.F[pp], p.Fv[pp], nf, p.Lptr,
+                                            fb, p.S[bpar], &c->s_count[bpar]);
+            else
+                capture_list<M, true, false>(p, sm, &c->slot[st % 3], p.F[pp], nullptr, nf, p.Lptr,
+                                             fb, p.S[bpar], &c->s_count[bpar]);
             if (!end_step(2, nf)) return;
             re = ldcg(&prev()->re_packed);
             pp ^= 1;
@@ -642,23 +998,37 @@ __global__ void __launch_bounds__(kThreads, 3)
         if (status) break;
 
         // ---- heavy relaxation from S with current t (sssp.py:218-227)
-        const unsigned long long scount = ldcg(&c->s_count[bser & 1]);
-        capture_step<M, false, false>(p, sm, &c->slot[st % 3], p.S, scount, L, H, p.Hptr, bser,
-                                      nullptr);
+        const unsigned long long scount = ldcg(&c->s_count[bpar]);
+        capture_list<M, false, false>(p, sm, &c->slot[st % 3], p.S[bpar], nullptr, scount, p.Hptr,
+                                      nullptr, nullptr, nullptr);
         if (!end_step(3, scount)) return;
         re = ldcg(&prev()->re_packed);
         const unsigned long long E = re & kMask33;
-        if (E > 0) {
+        if (E > pullH) {
+            escanned += (unsigned long long)p.Hpull.nnz;
+            ++npull;
+            const unsigned sl = (unsigned)(st % 3);
+            pull_step<M, false>(p, sm, &c->slot[sl], p.Hpull, p.Hedges, L, H, nullptr, nullptr);
+            if (!end_step(7, (unsigned long long)p.Hpull.nnz)) return;
+            const bool ovf = ldcg(&prev()->flags) & 1u;
+            commit_step<M, false>(p, sm, &c->slot[sl], p.Hpull, H, nullptr, nullptr);
+            if (!end_step(8, (unsigned long long)p.Hpull.nspan)) return;
+            if (ovf) {
+                status = kDevOverflow;
+                break;
+            }
+        } else if (E > 0) {
             escanned += E;
             relax_step<M, false>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Hedges, H,
-                                 nullptr, pser);
+                                 nullptr, nullptr);
             if (!end_step(4, E)) return;
             if (ldcg(&prev()->flags) & 1u) {
                 status = kDevOverflow;
                 break;
             }
         }
-        ++bser;
+        old_scount = scount;
+        bpar ^= 1;
         ++idx;
     }
 
@@ -673,10 +1043,17 @@ __global__ void __launch_bounds__(kThreads, 3)
 
     // ---- finalize: fp64 output, n_r, m_r, max distance (SsspResult, sssp.py:312-313)
     {
+        // retire the last bucket's S bits
+        const unsigned long long gt = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
+        for (unsigned long long i = gt; i < old_scount; i += (unsigned long long)gridDim.x * kThreads) {
+            const unsigned v = (unsigned)ldcg(p.S[bpar ^ 1] + i);
+            atomicAnd(p.sbits + (v >> 5), ~(1u << (v & 31)));
+        }
         unsigned long long cnt = 0, m = 0, mx = 0;
         const long long stride = (long long)gridDim.x * kThreads;
         for (long long v = (long long)blockIdx.x * kThreads + threadIdx.x; v < p.n; v += stride) {
-            const D d = __ldcg(p.dist + v);
+            const long long sv = __ldg(p.perm + v);
+            const D d = sv < n_scan ? __ldcg(p.dist + sv) : M::INF;
             if (d != M::INF) {
                 ++cnt;
                 m += (unsigned long long)(__ldg(p.indptr + v + 1) - __ldg(p.indptr + v));
@@ -697,6 +1074,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                 c->edges_scanned = escanned;
                 c->barriers = nbar;
                 c->steps = st;
+                c->pulls = npull;
                 if (!p.trace) c->last_bucket = idx;
                 c->status = 0;
             }
