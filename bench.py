@@ -134,6 +134,19 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the solver
+    kernel from the latest committed ncu --set full capture (profiles/)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", "r*_ncu_summary.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    return d.get("traffic_bytes_per_launch"), os.path.relpath(files[-1], REPO)
+
+
 def b_alg(m_r: int, n_r: int, n: int) -> int:
     """Algorithmic bytes per solve: one (col, w) pair per
     edge of a reached vertex, 2 int64 row offsets per reached vertex, one
@@ -315,6 +328,7 @@ def main():
     balg_mean = balg_tot / len(per_solve)
     peak, peak_kind = measured_peaks()
     achieved = balg_mean / (mean_kern * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic()
 
     # ---- delta sweep (informational)
     sweep = {}
@@ -418,7 +432,9 @@ def main():
                 "peak": peak,
                 "unit": "GB/s",
                 "frac": achieved / peak,
-                "traffic": None,
+                "traffic": traffic,
+                "traffic_unit": "bytes per launch (ncu dram read+write)",
+                "traffic_source": traffic_src,
                 "peak_kind": peak_kind,
                 "kernel": "ds::sssp_persistent_kernel<ModeFixed>",
                 "algorithmic_bytes_per_launch": balg_mean,
@@ -439,6 +455,7 @@ def main():
                 "kernel_ms_min": min(kern_ms),
                 "kernel_ms_max": max(kern_ms),
                 "prepare_ms": info.prepare_ms,
+                "pull_steps_mean": statistics.mean(p["pull_steps"] for p in per_solve),
                 "sweep": sweep,
             },
         }

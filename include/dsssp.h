@@ -84,6 +84,7 @@ typedef struct ds_stats {
     double kernel_ms;         /* device time of the solve (CUDA events)   */
     int32_t dist_mode;        /* mode that produced the result            */
     int32_t fallbacks;        /* 1 if fixed-point overflowed and f64 reran */
+    int64_t pull_steps;       /* relaxations run in pull (vxm) form       */
 } ds_stats;
 
 /* Upload a CSR adjacency (rows = out-edges).  indptr: n+1 int64; col: nnz

@@ -51,6 +51,7 @@ class Stats(ctypes.Structure):
         ("kernel_ms", ctypes.c_double),
         ("dist_mode", ctypes.c_int32),
         ("fallbacks", ctypes.c_int32),
+        ("pull_steps", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

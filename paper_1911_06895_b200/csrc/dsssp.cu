@@ -394,31 +394,55 @@ __global__ void k_chunk_plan(const long long* cptr, long long n_nz, unsigned* ch
     }
 }
 
-// A^T == A test (the pull reads rows of A as columns of A^T): every row has
-// strictly increasing columns, and each (u, v, w) has a bit-identical (v, u, w).
-__global__ void k_check_symmetric(const long long* indptr, const int* col, const double* w,
-                                  long long n, int* bad) {
+// A^T == A test (the pull reads rows of A as columns of A^T): the multiset of
+// (u, v, w) triples equals the multiset of (v, u, w) iff the graph is
+// symmetric with symmetric weights.  Compared through two independent 64-bit
+// sums of a strong mix of each triple (collision odds ~2^-128): one coalesced
+// pass over the edges instead of a search per edge.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x ^= x >> 33;
+    x *= 0xFF51AFD7ED558CCDull;
+    x ^= x >> 33;
+    x *= 0xC4CEB9FE1A85EC53ull;
+    x ^= x >> 33;
+    return x;
+}
+__device__ __forceinline__ void triple_hash(unsigned long long a, unsigned long long b,
+                                            unsigned long long w, unsigned long long& h1,
+                                            unsigned long long& h2) {
+    const unsigned long long k = (a << 32) | b;
+    h1 = mix64(k ^ mix64(w + 0x9E3779B97F4A7C15ull));
+    h2 = mix64((k * 0xD6E8FEB86659FD93ull) ^ mix64(w ^ 0x632BE59BD9B4E019ull) ^ 0x5851F42D4C957F2Dull);
+}
+__global__ void k_symmetry_sums(const long long* indptr, const int* col, const double* w, long long n,
+                                unsigned long long* sums) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long f1 = 0, f2 = 0, r1 = 0, r2 = 0;
     for (long long u = warp; u < n; u += nwarps) {
         const long long a = indptr[u], b = indptr[u + 1];
         for (long long e = a + lane; e < b; e += 32) {
-            const int v = col[e];
-            if (e + 1 < b && col[e + 1] <= v) {
-                atomicOr(bad, 1);
-                continue;
-            }
-            long long lo = indptr[v], hi = indptr[v + 1];
-            while (lo < hi) {  // binary search for u in row v
-                const long long mid = (lo + hi) >> 1;
-                if (col[mid] < u) lo = mid + 1;
-                else hi = mid;
-            }
-            if (lo >= indptr[v + 1] || col[lo] != u ||
-                __double_as_longlong(w[lo]) != __double_as_longlong(w[e]))
-                atomicOr(bad, 1);
+            const unsigned long long v = (unsigned)col[e];
+            const unsigned long long wb = (unsigned long long)__double_as_longlong(w[e]);
+            unsigned long long h1, h2;
+            triple_hash((unsigned long long)u, v, wb, h1, h2);
+            f1 += h1;
+            f2 += h2;
+            triple_hash(v, (unsigned long long)u, wb, h1, h2);
+            r1 += h1;
+            r2 += h2;
         }
+    }
+    f1 = warp_sum(f1);
+    f2 = warp_sum(f2);
+    r1 = warp_sum(r1);
+    r2 = warp_sum(r2);
+    if (lane == 0) {
+        atomicAdd(sums + 0, f1);
+        atomicAdd(sums + 1, f2);
+        atomicAdd(sums + 2, r1);
+        atomicAdd(sums + 3, r2);
     }
 }
 
@@ -651,16 +675,17 @@ static int build_plan(ds_graph* g, const long long* ptr, long long nnz, ds_graph
 }
 
 static int check_symmetric(ds_graph* g) {
-    int* bad = reinterpret_cast<int*>(g->pstat);
-    CK(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
+    unsigned long long* sums = reinterpret_cast<unsigned long long*>(g->pstat);  // 4 words
+    static_assert(sizeof(PrepStats) >= 4 * sizeof(unsigned long long), "scratch too small");
+    CK(cudaMemsetAsync(sums, 0, 4 * sizeof(unsigned long long), g->stream));
     if (g->nnz > 0)
-        k_check_symmetric<<<(unsigned)(g->nsm * 16), 256, 0, g->stream>>>(g->indptr, g->col, g->w, g->n,
-                                                                          bad);
+        k_symmetry_sums<<<(unsigned)(g->nsm * 16), 256, 0, g->stream>>>(g->indptr, g->col, g->w, g->n,
+                                                                        sums);
     CK(cudaGetLastError());
-    int h = 0;
-    CK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    unsigned long long h[4];
+    CK(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
-    g->symmetric = (h == 0);
+    g->symmetric = (h[0] == h[2] && h[1] == h[3]);
     return DS_OK;
 }
 
@@ -1098,6 +1123,7 @@ extern "C" int ds_sssp(ds_graph* g, int64_t source, double delta, uint32_t flags
         stats->kernel_ms = ms;
         stats->dist_mode = g->mode;
         stats->fallbacks = fallbacks;
+        stats->pull_steps = (int64_t)c.pulls;
     }
     return DS_OK;
 }

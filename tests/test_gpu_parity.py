@@ -245,3 +245,20 @@ def test_rmat20_fixed_vs_f64_and_dijkstra():
     want = oracle.dijkstra(g.n, indptr, col, val, s)
     assert bits_equal(fixed, want)
     g.close()
+
+
+def test_pull_path_used_and_exact_on_symmetric_graphs():
+    a = graphs.rmat(16, seed=3, weight_seed=4)
+    g = DeviceGraph.from_matrix(a)
+    s = graphs.pick_sources(a.indptr, 1, seed=5)[0]
+    st = _dense_check(g, a, s, 0.1, max(1, oracle.max_threads()))
+    assert st.pull_steps > 0
+    g.close()
+
+
+def test_directed_graph_never_pulls():
+    a = graphs.erdos_renyi(1024, seed=0)  # directed: A^T != A
+    g = DeviceGraph.from_matrix(a)
+    st = _dense_check(g, a, 0, 3.0, 1)
+    assert st.pull_steps == 0
+    g.close()

@@ -1,7 +1,7 @@
 """Per-step timeline of one solve (DS_TRACE=1): time per step kind."""
 import os, sys, ctypes, collections
 os.environ["DS_TRACE"] = "1"
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_1911_06895_b200 import DeviceGraph, graphs, _lib
 
