@@ -18,6 +18,9 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libdsssp.so")
+# variant with the pull (vxm) relaxations compiled in (opt-in)
+LIB_PULL = os.path.join(LIB_DIR, "libdsssp_pull.so")
+VARIANTS = {LIB: [], LIB_PULL: ["-DDS_PULL_LIGHT=1", "-DDS_PULL_HEAVY=1"]}
 SOURCES = ["dsssp.cu", "gen.cu"]
 HEADERS = ["common.cuh", "sssp_kernel.cuh"]
 
@@ -38,25 +41,26 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found; the CUDA toolkit is required to build libdsssp.so")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(REPO, "include", "dsssp.h"))
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    tmp = LIB + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    for lib, extra in VARIANTS.items():
+        if not force and not _stale(lib):
+            continue
+        tmp = lib + ".tmp"
+        cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, lib)
     return LIB
 
 

@@ -138,6 +138,16 @@ constexpr int kQueue = 256;       // per-warp append staging (overflow spills to
 #define DS_PRECHECK_L1 1
 #endif
 constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
+// Pull (vxm) forms compiled into the solver.  Both are correct (parity tests
+// run with them on) but on R-MAT 24 they cost more than they save: the extra
+// code raises register pressure (spills) in every step of this persistent
+// kernel, so they are opt-in builds (-DDS_PULL_LIGHT=1 / -DDS_PULL_HEAVY=1).
+#ifndef DS_PULL_LIGHT
+#define DS_PULL_LIGHT 0
+#endif
+#ifndef DS_PULL_HEAVY
+#define DS_PULL_HEAVY 0
+#endif
 
 struct StepSlot {
     unsigned long long re_packed;     // capture: reserved (entries << 33) | edges
@@ -958,7 +968,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             bool vals = false;
             const unsigned long long E = re & kMask33;
             unsigned* fb = p.fbits[phases & 1];
-            if (E > pullL) {
+            if (DS_PULL_LIGHT && E > pullL) {
                 escanned += (unsigned long long)p.Lpull.nnz;
                 ++npull;
                 const unsigned sl = (unsigned)(st % 3);
@@ -1004,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         if (!end_step(3, scount)) return;
         re = ldcg(&prev()->re_packed);
         const unsigned long long E = re & kMask33;
-        if (E > pullH) {
+        if (DS_PULL_HEAVY && E > pullH) {
             escanned += (unsigned long long)p.Hpull.nnz;
             ++npull;
             const unsigned sl = (unsigned)(st % 3);
