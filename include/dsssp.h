@@ -143,6 +143,32 @@ int ds_gen_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, uint64_t weig
  * col nnz int32, val nnz float32 (weights must be float32-exact). */
 int ds_graph_download(ds_graph* g, int64_t* indptr, int32_t* col, float* val);
 
+/* ------------------------------------------------------------------------
+ * Partitioned solver: one shard per rank / GPU.  A shard
+ * owns the input-id range [v0, v0 + n_local) and stores the edges whose
+ * TARGET it owns as a CSR over all n_global sources (col = local target id).
+ * The host exchanges frontiers between ranks (all-gather) once per phase;
+ * paper_1911_06895_b200/distributed.py drives the protocol.  Buffers passed
+ * to scan/s_add/relax are device pointers; values are distances widened to
+ * u64 (fixed-point integers or binary64 bit patterns). */
+typedef struct ds_shard ds_shard;
+
+int ds_shard_create(int64_t n_global, int64_t v0, int64_t n_local, int64_t nnz,
+                    const int64_t* indptr, const int32_t* col_local, const double* val,
+                    int device, void* stream, ds_shard** out);
+void ds_shard_destroy(ds_shard* s);
+/* out5 = {min light weight bits, max weight bits, max fraction bits, nnz_L, nnz_H} */
+int ds_shard_probe(ds_shard* s, double delta, uint64_t* out5);
+int ds_shard_prepare(ds_shard* s, double delta, int mode, int frac_bits);
+int ds_shard_begin(ds_shard* s, int64_t source);
+int ds_shard_scan(ds_shard* s, uint64_t L, uint64_t H, int32_t* out_ids, uint64_t* out_vals,
+                  int64_t* count, uint64_t* next_min);
+int ds_shard_s_add(ds_shard* s, const int32_t* ids, const uint64_t* vals, int64_t count);
+int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const uint64_t* vals, int64_t count,
+                   uint64_t H, int32_t* out_ids, uint64_t* out_vals, int64_t* out_count,
+                   int32_t* overflow);
+int ds_shard_result(ds_shard* s, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,8 @@ EXPORTS = (
     "ds_graph_create", "ds_graph_prepare", "ds_sssp", "ds_result_dense", "ds_result_sparse",
     "ds_export_split", "ds_graph_set_stream", "ds_graph_size", "ds_graph_destroy",
     "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download", "ds_debug_trace",
+    "ds_shard_create", "ds_shard_destroy", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",
+    "ds_shard_scan", "ds_shard_s_add", "ds_shard_relax", "ds_shard_result",
 )
 
 
@@ -105,6 +107,23 @@ def lib():
         L.ds_graph_download.argtypes = [_vp, _vp, _vp, _vp]
         L.ds_debug_trace.argtypes = [_vp, _vp, _i64]
         L.ds_debug_trace.restype = _i64
+        u64 = ctypes.c_uint64
+        L.ds_shard_create.argtypes = [_i64, _i64, _i64, _i64, _vp, _vp, _vp, ctypes.c_int, _vp,
+                                      ctypes.POINTER(_vp)]
+        L.ds_shard_destroy.argtypes = [_vp]
+        L.ds_shard_destroy.restype = None
+        L.ds_shard_probe.argtypes = [_vp, ctypes.c_double, _vp]
+        L.ds_shard_prepare.argtypes = [_vp, ctypes.c_double, ctypes.c_int, ctypes.c_int]
+        L.ds_shard_begin.argtypes = [_vp, _i64]
+        L.ds_shard_scan.argtypes = [_vp, u64, u64, _vp, _vp, ctypes.POINTER(_i64),
+                                    ctypes.POINTER(u64)]
+        L.ds_shard_s_add.argtypes = [_vp, _vp, _vp, _i64]
+        L.ds_shard_relax.argtypes = [_vp, ctypes.c_int, _vp, _vp, _i64, u64, _vp, _vp,
+                                     ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int32)]
+        L.ds_shard_result.argtypes = [_vp, _vp]
+        for name in ("ds_shard_create", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",
+                     "ds_shard_scan", "ds_shard_s_add", "ds_shard_relax", "ds_shard_result"):
+            getattr(L, name).restype = ctypes.c_int
         for name in ("ds_graph_create", "ds_graph_prepare", "ds_sssp", "ds_result_dense",
                      "ds_result_sparse", "ds_export_split", "ds_graph_set_stream",
                      "ds_graph_size", "ds_gen_rmat", "ds_graph_download"):
