@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also time delta in {0.05, 0.25}")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="1-D vertex-partitioned solver across the ranks (SURVEY.md 8(e)): every "
+                         "source is solved jointly, one frontier all-gather per phase")
     return ap.parse_args()
 
 
@@ -240,12 +243,90 @@ def reference_arm(args):
     return 0
 
 
+# ------------------------------------------------------------------ partitioned arm
+
+def partitioned_arm(args):
+    """Every source solved jointly by all ranks: rank r owns a contiguous id
+    range and the edges into it; one NCCL all-gather of the frontier per light
+    phase.  Timed with CUDA events, max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1911_06895_b200 import DeviceGraph, graphs
+    from paper_1911_06895_b200.distributed import (DeviceShard, PartitionedDeltaStepping,
+                                                   partition_bounds)
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=rank, world_size=ws,
+                            device_id=torch.device(f"cuda:{local}"))
+    g = DeviceGraph.rmat(args.scale, args.edge_factor, 1, 2, device=local)
+    n, nnz = g.n, g.nnz
+    indptr = g.download()[0]
+    deg = np.diff(indptr)
+    b = partition_bounds(n, ws)
+    shard = DeviceShard.from_graph(g, b[rank], b[rank + 1])
+    g.close()
+    solver = PartitionedDeltaStepping(shard, n, dist, "cuda")
+    pool = graphs.pick_sources(indptr, args.sources, seed=7)
+    mydeg = deg[b[rank]:b[rank + 1]]
+
+    def batch(step):
+        return [pool[(step * args.batch + j) % len(pool)] for j in range(args.batch)]
+
+    for w in range(args.warmup):
+        for s in batch(w):
+            solver.solve(s, args.delta)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    m_local, phases, exch = 0, [], 0
+    e0.record()
+    for k in range(args.steps):
+        for s in batch(args.warmup + k):
+            r = solver.solve(s, args.delta)
+            m_local += int(mydeg[np.isfinite(r.local)].sum())
+            phases.append(r.inner_phases)
+            exch += r.exchanged
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    m = torch.tensor([float(m_local)], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(m)
+    t_ms = float(t.item())
+    value = float(m.item()) / (t_ms * 1e-3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32 fixed-point (exact f64)",
+            "data": "synthetic (seeded R-MAT, generated on device)",
+            "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_delta{args.delta}",
+                       "n": n, "nnz": nnz, "sources_per_step": args.batch,
+                       "parallelism": f"1-D vertex partition x{ws}, NCCL all-gather per phase"},
+            "gpu_launches": None,
+            "solver": {"phases_mean": statistics.mean(phases),
+                       "frontier_entries_exchanged_per_source": exch / max(1, len(phases))},
+        }), flush=True)
+    shard.close()
+    dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------------ GPU arm
 
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.partitioned:
+        return partitioned_arm(args)
 
     import numpy as np
     import torch

@@ -168,6 +168,8 @@ int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const uint64_t* v
                    uint64_t H, int32_t* out_ids, uint64_t* out_vals, int64_t* out_count,
                    int32_t* overflow);
 int ds_shard_result(ds_shard* s, double* out);
+/* Shard [v0, v1) cut on the device from a resident graph handle. */
+int ds_shard_from_graph(ds_graph* g, int64_t v0, int64_t v1, ds_shard** out);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ EXPORTS = (
     "ds_export_split", "ds_graph_set_stream", "ds_graph_size", "ds_graph_destroy",
     "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download", "ds_debug_trace",
     "ds_shard_create", "ds_shard_destroy", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",
-    "ds_shard_scan", "ds_shard_s_add", "ds_shard_relax", "ds_shard_result",
+    "ds_shard_scan", "ds_shard_s_add", "ds_shard_relax", "ds_shard_result", "ds_shard_from_graph",
 )
 
 
@@ -121,6 +121,8 @@ def lib():
         L.ds_shard_relax.argtypes = [_vp, ctypes.c_int, _vp, _vp, _i64, u64, _vp, _vp,
                                      ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int32)]
         L.ds_shard_result.argtypes = [_vp, _vp]
+        L.ds_shard_from_graph.argtypes = [_vp, _i64, _i64, ctypes.POINTER(_vp)]
+        L.ds_shard_from_graph.restype = ctypes.c_int
         for name in ("ds_shard_create", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",
                      "ds_shard_scan", "ds_shard_s_add", "ds_shard_relax", "ds_shard_result"):
             getattr(L, name).restype = ctypes.c_int

@@ -1314,3 +1314,16 @@ extern "C" int64_t ds_debug_trace(ds_graph* g, uint64_t* out, int64_t cap) {
         return 0;
     return m;
 }
+
+int ds_internal_graph_csr(ds_graph* g, long long** indptr, int** col, double** w, long long* n,
+                          long long* nnz, int* device, void** stream) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    *indptr = g->indptr;
+    *col = g->col;
+    *w = g->w;
+    *n = g->n;
+    *nnz = g->nnz;
+    *device = g->device;
+    *stream = (void*)g->stream;
+    return DS_OK;
+}

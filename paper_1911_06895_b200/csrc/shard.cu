@@ -574,3 +574,93 @@ extern "C" int ds_shard_result(ds_shard* s, double* out) {
     }
     return DS_OK;
 }
+
+// ---------------------------------------------------------------- shard from a device graph
+
+int ds_internal_graph_csr(ds_graph* g, long long** indptr, int** col, double** w, long long* n,
+                          long long* nnz, int* device, void** stream);
+
+namespace {
+__global__ void k_slice_count(const long long* indptr, const int* col, long long n, int v0, int v1,
+                              long long* counts) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long r = warp; r < n; r += nwarps) {
+        unsigned long long c = 0;
+        for (long long e = indptr[r] + lane; e < indptr[r + 1]; e += 32) {
+            const int v = col[e];
+            c += (v >= v0 && v < v1);
+        }
+        c = warp_sum(c);
+        if (lane == 0) counts[r] = (long long)c;
+    }
+}
+
+__global__ void k_slice_scatter(const long long* indptr, const int* col, const double* w, long long n,
+                                int v0, int v1, const long long* optr, int* ocol, double* ow) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (long long r = warp; r < n; r += nwarps) {
+        long long o = optr[r];
+        for (long long e0 = indptr[r]; e0 < indptr[r + 1]; e0 += 32) {
+            const long long e = e0 + lane;
+            const int v = e < indptr[r + 1] ? col[e] : -1;
+            const bool keep = v >= v0 && v < v1;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const long long k = o + __popc(m & lt);
+                ocol[k] = v - v0;
+                ow[k] = w[e];
+            }
+            o += __popc(m);
+        }
+    }
+}
+}  // namespace
+
+// Shard [v0, v1) of a graph already resident on the device (no host copy).
+extern "C" int ds_shard_from_graph(ds_graph* g, int64_t v0, int64_t v1, ds_shard** out) {
+    long long *indptr = nullptr, n = 0, nnz = 0;
+    int* col = nullptr;
+    double* w = nullptr;
+    int device = 0;
+    void* stream = nullptr;
+    int rc = ds_internal_graph_csr(g, &indptr, &col, &w, &n, &nnz, &device, &stream);
+    if (rc) return rc;
+    if (!(0 <= v0 && v0 <= v1 && v1 <= n)) return ds_internal_set_err(DS_EINVAL, "bad shard range");
+    cudaSetDevice(device);
+    cudaStream_t st = (cudaStream_t)stream;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    long long *counts = nullptr, *optr = nullptr;
+    int* ocol = nullptr;
+    double* ow = nullptr;
+    void* tmp = nullptr;
+    size_t bytes = 0;
+    long long m = 0;
+    SCK(cudaMalloc(&counts, sizeof(long long) * (n + 1)));
+    SCK(cudaMalloc(&optr, sizeof(long long) * (n + 1)));
+    k_slice_count<<<nsm * 16, 256, 0, st>>>(indptr, col, n, (int)v0, (int)v1, counts);
+    SCK(cudaGetLastError());
+    SCK(cudaMemsetAsync(optr, 0, sizeof(long long), st));
+    SCK(cub::DeviceScan::InclusiveSum(nullptr, bytes, counts, optr + 1, n, st));
+    SCK(cudaMalloc(&tmp, bytes));
+    SCK(cub::DeviceScan::InclusiveSum(tmp, bytes, counts, optr + 1, n, st));
+    SCK(cudaMemcpyAsync(&m, optr + n, sizeof(long long), cudaMemcpyDeviceToHost, st));
+    SCK(cudaStreamSynchronize(st));
+    SCK(cudaMalloc(&ocol, sizeof(int) * (m > 0 ? m : 1)));
+    SCK(cudaMalloc(&ow, sizeof(double) * (m > 0 ? m : 1)));
+    k_slice_scatter<<<nsm * 16, 256, 0, st>>>(indptr, col, w, n, (int)v0, (int)v1, optr, ocol, ow);
+    SCK(cudaGetLastError());
+    SCK(cudaStreamSynchronize(st));
+    rc = ds_shard_create(n, v0, v1 - v0, m, (const int64_t*)optr, ocol, ow, device, stream, out);
+    cudaFree(counts);
+    cudaFree(optr);
+    cudaFree(ocol);
+    cudaFree(ow);
+    cudaFree(tmp);
+    return rc;
+}

@@ -105,6 +105,23 @@ class DeviceShard:
         self.out_ids = torch.empty(m, dtype=torch.int32, device=self.device)
         self.out_vals = torch.empty(m, dtype=torch.int64, device=self.device)
 
+    @classmethod
+    def from_graph(cls, graph, v0: int, v1: int) -> "DeviceShard":
+        """Cut the shard [v0, v1) on the device from a resident `DeviceGraph`."""
+        import torch
+
+        self = cls.__new__(cls)
+        self.torch = torch
+        self.n, self.v0, self.nl = int(graph.n), int(v0), int(v1 - v0)
+        self.device = torch.device("cuda", graph.device)
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib().ds_shard_from_graph(graph._handle(), int(v0), int(v1), ctypes.byref(h)))
+        self._h = h
+        m = max(self.nl, 1)
+        self.out_ids = torch.empty(m, dtype=torch.int32, device=self.device)
+        self.out_vals = torch.empty(m, dtype=torch.int64, device=self.device)
+        return self
+
     def close(self):
         if self._h.value:
             _lib.lib().ds_shard_destroy(self._h)
