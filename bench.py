@@ -272,14 +272,14 @@ def partitioned_arm(args):
     g.close()
     solver = PartitionedDeltaStepping(shard, n, dist, "cuda")
     pool = graphs.pick_sources(indptr, args.sources, seed=7)
-    mydeg = deg[b[rank]:b[rank + 1]]
+    mydeg = torch.from_numpy(deg[b[rank]:b[rank + 1]].astype(np.int64)).to(f"cuda:{local}")
 
     def batch(step):
         return [pool[(step * args.batch + j) % len(pool)] for j in range(args.batch)]
 
     for w in range(args.warmup):
         for s in batch(w):
-            solver.solve(s, args.delta)
+            solver.solve(s, args.delta, on_device=True)
     dist.barrier()
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -288,8 +288,8 @@ def partitioned_arm(args):
     e0.record()
     for k in range(args.steps):
         for s in batch(args.warmup + k):
-            r = solver.solve(s, args.delta)
-            m_local += int(mydeg[np.isfinite(r.local)].sum())
+            r = solver.solve(s, args.delta, on_device=True)
+            m_local += int(mydeg[torch.isfinite(r.local)].sum().item())
             phases.append(r.inner_phases)
             exch += r.exchanged
     e1.record()

@@ -12,8 +12,9 @@
 // termination) are made identically on every rank from all-reduced scalars,
 // so distances and counters equal the single-GPU solver's.
 //
-// The step kernels are plain grid-stride launches driven from the host (one
-// exchange per phase is a host-visible synchronisation point anyway).
+// The step kernels are plain launches driven from the host (one exchange per
+// phase is a host-visible synchronisation point anyway); the push reuses the
+// single-GPU solver's edge-balanced capture/relax device code.
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
@@ -67,6 +68,13 @@ struct ds_shard {
     int* tmp_ids = nullptr;             // nl
     unsigned long long* tmp_vals = nullptr;  // nl
     long long* cnt_scratch = nullptr;
+    // edge-balanced push (the single-GPU solver's capture/relax machinery)
+    long long* Rpre = nullptr;   // n entries
+    long long* Rbase = nullptr;  // n entries
+    void* Rd = nullptr;          // n entries of D
+    unsigned* chunk_start = nullptr;
+    StepSlot* slot = nullptr;
+    int grid_fixed = 0, grid_f64 = 0;
 };
 
 namespace {
@@ -135,54 +143,6 @@ __global__ void k_shard_gather_s(const int* slist, long long count, const unsign
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
          i += (long long)gridDim.x * blockDim.x)
         out_vals[i] = sval[slist[i]];
-}
-
-// Warp per source entry, lanes stride over its (local-target) edges.
-template <class M, bool LIGHT>
-__global__ void k_shard_push(const int* ids, const unsigned long long* vals, long long count,
-                             const long long* ptr, const typename M::Edge* edges,
-                             typename M::D* dist, typename M::D H, unsigned* fbits, int* out_local,
-                             unsigned long long* counters) {
-    using D = typename M::D;
-    const int lane = threadIdx.x & 31;
-    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    bool overflow = false;
-    const unsigned long long pol = evict_first_policy();
-    for (long long i = warp; i < count; i += nwarps) {
-        const int u = ids[i];
-        const D du = (D)vals[i];
-        const long long a = ptr[u], b = ptr[u + 1];
-        for (long long e0 = a; e0 < b; e0 += 32) {
-            const long long e = e0 + lane;
-            bool want = false;
-            unsigned v = 0;
-            if (e < b) {
-                const typename M::Edge ed = M::load(edges + e, pol);
-                D nd;
-                if (M::add(du, ed, nd)) {
-                    v = M::col(ed);
-                    if (nd < dist[v]) {
-                        const D old = atomicMin(dist + v, nd);
-                        if (LIGHT) want = nd < old && nd < H && claim_bit(fbits, v);
-                    }
-                } else {
-                    overflow = true;
-                }
-            }
-            if (LIGHT) {
-                const unsigned m = __ballot_sync(0xffffffffu, want);
-                if (m) {
-                    unsigned long long base = 0;
-                    const int leader = __ffs(m) - 1;
-                    if (lane == leader) base = atomicAdd(&counters[0], (unsigned long long)__popc(m));
-                    base = __shfl_sync(0xffffffffu, base, leader);
-                    if (want) out_local[base + __popc(m & ((1u << lane) - 1u))] = (int)v;
-                }
-            }
-        }
-    }
-    if (overflow) atomicOr(reinterpret_cast<unsigned*>(&counters[3]), 1u);
 }
 
 // next frontier: local ids -> global ids + final values; clear their dedup bits
@@ -292,6 +252,46 @@ __global__ void k_shard_scatter(long long n, const long long* indptr, const int*
     }
 }
 
+// Capture of an exchanged frontier (global source ids + u64-widened values):
+// degrees from the shard's CSR rows, entries + chunk map for relax_step.
+template <class M>
+__global__ void __launch_bounds__(kThreads) k_shard_capture(const KParams<M> p, StepSlot* slot,
+                                                            const int* ids,
+                                                            const unsigned long long* vals,
+                                                            long long count, const long long* ptr) {
+    using D = typename M::D;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const unsigned long long per_chunk = 32ull * kListPer;
+    const unsigned long long nchunk = ((unsigned long long)count + per_chunk - 1) / per_chunk;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    for (unsigned long long c = gw; c < nchunk; c += nw) {
+        D dv[kListPer];
+        long long off[kListPer], deg[kListPer];
+#pragma unroll
+        for (int j = 0; j < kListPer; ++j) {
+            const unsigned long long idx = c * per_chunk + lane + 32ull * j;
+            const bool in = idx < (unsigned long long)count;
+            const int u = in ? ids[idx] : 0;
+            dv[j] = in ? (D)vals[idx] : (D)0;
+            off[j] = in ? __ldg(ptr + u) : 0;
+            deg[j] = in ? __ldg(ptr + u + 1) - off[j] : 0;
+        }
+        capture_emit<M, kListPer>(p, slot, lane, dv, off, deg);
+    }
+}
+
+template <class M, bool LIGHT>
+__global__ void __launch_bounds__(kThreads) k_shard_relax(const KParams<M> p, StepSlot* slot,
+                                                          unsigned long long E, unsigned long long Rc,
+                                                          const typename M::Edge* edges,
+                                                          typename M::D H, int* out_list,
+                                                          unsigned* fbits) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<typename M::D>& sm = *reinterpret_cast<Smem<typename M::D>*>(smem_raw);
+    relax_step<M, LIGHT>(p, sm, slot, E, Rc, edges, H, out_list, fbits);
+}
+
 }  // namespace
 
 static unsigned sgrid(ds_shard* s) { return (unsigned)(s->nsm * 8); }
@@ -344,6 +344,19 @@ extern "C" int ds_shard_create(int64_t n_global, int64_t v0, int64_t n_local, in
     SCF(cudaMalloc(&s->tmp_ids, sizeof(int) * nl1));
     SCF(cudaMalloc(&s->tmp_vals, sizeof(unsigned long long) * nl1));
     SCF(cudaMalloc(&s->cnt_scratch, sizeof(long long) * 2 * (n_global + 1)));
+    SCF(cudaMalloc(&s->Rpre, sizeof(long long) * n_global));
+    SCF(cudaMalloc(&s->Rbase, sizeof(long long) * n_global));
+    SCF(cudaMalloc(&s->Rd, sizeof(unsigned long long) * n_global));
+    SCF(cudaMalloc(&s->chunk_start, sizeof(unsigned) * (std::max<long long>(nnz, 1LL) / kChunk + 4)));
+    SCF(cudaMalloc(&s->slot, sizeof(StepSlot)));
+    SCF(cudaFuncSetAttribute(k_shard_relax<ModeFixed, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem<unsigned>)));
+    SCF(cudaFuncSetAttribute(k_shard_relax<ModeFixed, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem<unsigned>)));
+    SCF(cudaFuncSetAttribute(k_shard_relax<ModeF64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem<unsigned long long>)));
+    SCF(cudaFuncSetAttribute(k_shard_relax<ModeF64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem<unsigned long long>)));
     SCF(cudaMemsetAsync(s->fbits, 0, sizeof(unsigned) * (nl1 / 32 + 1), s->stream));
     SCF(cudaMemsetAsync(s->sbits, 0, sizeof(unsigned) * (n_global / 32 + 1), s->stream));
     SCF(cudaStreamSynchronize(s->stream));
@@ -358,7 +371,7 @@ extern "C" void ds_shard_destroy(ds_shard* s) {
     cudaStreamSynchronize(s->stream);
     void* ptrs[] = {s->indptr, s->col, s->w, s->Lptr, s->Hptr, s->Ledges, s->Hedges, s->dist,
                     s->fbits, s->sbits, s->sval, s->slist, s->counters, s->tmp_ids, s->tmp_vals,
-                    s->cnt_scratch};
+                    s->cnt_scratch, s->Rpre, s->Rbase, s->Rd, s->chunk_start, s->slot};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;
@@ -483,6 +496,52 @@ extern "C" int ds_shard_s_add(ds_shard* s, const int32_t* ids, const uint64_t* v
     return DS_OK;
 }
 
+
+// Edge-balanced push of (ids, vals) through the shard's light or heavy CSR.
+// Light: the owned part of the next frontier lands in s->tmp_ids and its size
+// in *nf.  Returns DS_OK; *ovf gets the fixed-point overflow flag.
+template <class M>
+static int shard_push(ds_shard* s, bool light, const int* ids, const unsigned long long* vals,
+                      long long count, typename M::D H, long long* nf, int* ovf) {
+    KParams<M> p{};
+    p.dist = (typename M::D*)s->dist;
+    p.Rpre = s->Rpre;
+    p.Rbase = s->Rbase;
+    p.Rd = (typename M::D*)s->Rd;
+    p.chunk_start = s->chunk_start;
+    SCK(cudaMemsetAsync(s->slot, 0, sizeof(StepSlot), s->stream));
+    const unsigned grid = (unsigned)(s->nsm * 4);
+    k_shard_capture<M><<<grid, kThreads, 0, s->stream>>>(p, s->slot, ids, vals, count,
+                                                         light ? s->Lptr : s->Hptr);
+    SCK(cudaGetLastError());
+    StepSlot h{};
+    SCK(cudaMemcpyAsync(&h, s->slot, sizeof(StepSlot), cudaMemcpyDeviceToHost, s->stream));
+    SCK(cudaStreamSynchronize(s->stream));
+    const unsigned long long E = h.re_packed & kMask33, Rc = h.re_packed >> kPackShift;
+    *nf = 0;
+    *ovf = 0;
+    if (E == 0) return DS_OK;
+    const size_t smem = sizeof(Smem<typename M::D>);
+    int occ = 1;
+    if (light)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_shard_relax<M, true>, kThreads, smem);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_shard_relax<M, false>, kThreads, smem);
+    const unsigned rgrid = (unsigned)(s->nsm * std::max(occ, 1));
+    if (light)
+        k_shard_relax<M, true><<<rgrid, kThreads, smem, s->stream>>>(
+            p, s->slot, E, Rc, (const typename M::Edge*)s->Ledges, H, s->tmp_ids, s->fbits);
+    else
+        k_shard_relax<M, false><<<rgrid, kThreads, smem, s->stream>>>(
+            p, s->slot, E, Rc, (const typename M::Edge*)s->Hedges, H, nullptr, nullptr);
+    SCK(cudaGetLastError());
+    SCK(cudaMemcpyAsync(&h, s->slot, sizeof(StepSlot), cudaMemcpyDeviceToHost, s->stream));
+    SCK(cudaStreamSynchronize(s->stream));
+    *nf = (long long)h.append_count;
+    *ovf = (int)(h.flags & 1u);
+    return DS_OK;
+}
+
 // Light relaxation of an exchanged frontier (global ids + captured values)
 // into the owned targets; the owned part of the next frontier comes back as
 // global ids + final values (out buffers hold nl entries).  heavy=1 relaxes
@@ -492,51 +551,34 @@ extern "C" int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const 
                               int64_t* out_count, int32_t* overflow) {
     if (!s) return ds_internal_set_err(DS_EINVAL, "null shard");
     cudaSetDevice(s->device);
-    unsigned long long z[4] = {0, 0, 0, 0};
-    SCK(cudaMemcpyAsync(s->counters, z, sizeof(unsigned long long), cudaMemcpyHostToDevice, s->stream));
-    SCK(cudaMemcpyAsync(s->counters + 3, z, sizeof(unsigned long long), cudaMemcpyHostToDevice, s->stream));
-    const unsigned grid = (unsigned)(s->nsm * 16);
     const bool fx = s->mode == DS_MODE_FIXED32;
+    long long nf = 0;
+    int ovf = 0, rc = DS_OK;
     if (heavy) {
         const long long sc = s->scount;
         if (sc > 0) {
-            k_shard_gather_s<<<sgrid(s), kT, 0, s->stream>>>(s->slist, sc, s->sval,
-                                                              (unsigned long long*)s->cnt_scratch);
-            if (fx)
-                k_shard_push<ModeFixed, false><<<grid, kT, 0, s->stream>>>(
-                    s->slist, (const unsigned long long*)s->cnt_scratch, sc, s->Hptr,
-                    (const uint2*)s->Hedges, (unsigned*)s->dist, 0u, nullptr, nullptr, s->counters);
-            else
-                k_shard_push<ModeF64, false><<<grid, kT, 0, s->stream>>>(
-                    s->slist, (const unsigned long long*)s->cnt_scratch, sc, s->Hptr,
-                    (const EdgeF64*)s->Hedges, (unsigned long long*)s->dist, 0ull, nullptr, nullptr,
-                    s->counters);
+            unsigned long long* sv = (unsigned long long*)s->cnt_scratch;
+            k_shard_gather_s<<<sgrid(s), kT, 0, s->stream>>>(s->slist, sc, s->sval, sv);
+            SCK(cudaGetLastError());
+            rc = fx ? shard_push<ModeFixed>(s, false, s->slist, sv, sc, 0u, &nf, &ovf)
+                    : shard_push<ModeF64>(s, false, s->slist, sv, sc, 0ull, &nf, &ovf);
+            if (rc) return rc;
             k_shard_s_clear<<<sgrid(s), kT, 0, s->stream>>>(s->slist, sc, s->sbits);
+            SCK(cudaGetLastError());
+            SCK(cudaStreamSynchronize(s->stream));
         }
         s->scount = 0;
-        SCK(cudaGetLastError());
-        SCK(cudaMemcpyAsync(s->h_counters, s->counters, 4 * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, s->stream));
-        SCK(cudaStreamSynchronize(s->stream));
         if (out_count) *out_count = 0;
-        if (overflow) *overflow = (int)(s->h_counters[3] & 1u);
+        if (overflow) *overflow = ovf;
         return DS_OK;
     }
     if (count > 0) {
-        if (fx)
-            k_shard_push<ModeFixed, true><<<grid, kT, 0, s->stream>>>(
-                ids, (const unsigned long long*)vals, count, s->Lptr, (const uint2*)s->Ledges,
-                (unsigned*)s->dist, (unsigned)H, s->fbits, s->tmp_ids, s->counters);
-        else
-            k_shard_push<ModeF64, true><<<grid, kT, 0, s->stream>>>(
-                ids, (const unsigned long long*)vals, count, s->Lptr, (const EdgeF64*)s->Ledges,
-                (unsigned long long*)s->dist, H, s->fbits, s->tmp_ids, s->counters);
+        rc = fx ? shard_push<ModeFixed>(s, true, ids, (const unsigned long long*)vals, count,
+                                        (unsigned)H, &nf, &ovf)
+                : shard_push<ModeF64>(s, true, ids, (const unsigned long long*)vals, count, H, &nf,
+                                      &ovf);
+        if (rc) return rc;
     }
-    SCK(cudaGetLastError());
-    SCK(cudaMemcpyAsync(s->h_counters, s->counters, 4 * sizeof(unsigned long long),
-                        cudaMemcpyDeviceToHost, s->stream));
-    SCK(cudaStreamSynchronize(s->stream));
-    const long long nf = (long long)s->h_counters[0];
     if (nf > 0) {
         if (fx)
             k_shard_emit<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>(s->tmp_ids, nf, (const unsigned*)s->dist,
@@ -550,7 +592,7 @@ extern "C" int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const 
         SCK(cudaStreamSynchronize(s->stream));
     }
     *out_count = nf;
-    if (overflow) *overflow = (int)(s->h_counters[3] & 1u);
+    if (overflow) *overflow = ovf;
     return DS_OK;
 }
 

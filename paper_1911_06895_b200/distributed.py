@@ -141,7 +141,11 @@ class DeviceShard:
                 "nL": int(out[3]), "nH": int(out[4])}
 
     def prepare(self, delta: float, mode: int, frac: int) -> None:
+        key = (float(delta), int(mode), int(frac))
+        if getattr(self, "_prepared", None) == key:
+            return  # split cached per (delta, mode), like the single-GPU handle
         _lib.check(_lib.lib().ds_shard_prepare(self._h, float(delta), int(mode), int(frac)))
+        self._prepared = key
 
     def begin(self, source: int) -> None:
         _lib.check(_lib.lib().ds_shard_begin(self._h, int(source)))
@@ -173,8 +177,12 @@ class DeviceShard:
                                              ctypes.byref(oc), ctypes.byref(ov)))
         return bool(ov.value)
 
-    def result(self) -> np.ndarray:
-        out = np.empty(max(self.nl, 1), dtype=np.float64)
+    def result(self, on_device: bool = False):
+        """Owned float64 distances: numpy (host) or a torch tensor left on the GPU."""
+        if on_device:
+            out = self.torch.empty(max(self.nl, 1), dtype=self.torch.float64, device=self.device)
+        else:
+            out = np.empty(max(self.nl, 1), dtype=np.float64)
         _lib.check(_lib.lib().ds_shard_result(self._h, _ptr(out)))
         return out[: self.nl]
 
@@ -254,20 +262,31 @@ class PartitionedDeltaStepping:
         return mode, fb, self.n * per
 
     def solve(self, source: int, delta: float, skip_empty_buckets: bool = False,
-              force_f64: bool = False) -> ShardedResult:
+              force_f64: bool = False, on_device: bool = False) -> ShardedResult:
+        """Joint solve of one source.  `local` is numpy, or a device tensor
+        when on_device=True (no host copy of the distances)."""
         if not 0 <= source < self.n:
             raise ValueError(f"source {source} out of range for {self.n} vertices")
         if not (delta > 0) or not math.isfinite(delta):
             raise ValueError(f"delta must be a positive finite number, got {delta}")
-        mode, frac, ceiling = self._decide_mode(delta, force_f64)
-        res = self._run(source, delta, mode, frac, ceiling)
+        key = (float(delta), bool(force_f64))
+        if getattr(self, "_mode_key", None) != key:
+            self._mode = self._decide_mode(delta, force_f64)
+            self._mode_key = key
+        mode, frac, ceiling = self._mode
+        res = self._run(source, delta, mode, frac, ceiling, on_device)
         if res is None:  # a fixed-point sum overflowed on some rank: exact f64 rerun
             mode, frac, ceiling = self._decide_mode(delta, True)
-            res = self._run(source, delta, mode, frac, ceiling)
+            self._mode, self._mode_key = (mode, frac, ceiling), (float(delta), False)
+            res = self._run(source, delta, mode, frac, ceiling, on_device)
         local, phases, visited, exchanged = res
         R = self.pg.ReduceOp
-        fin = local[np.isfinite(local)]
-        mx = float(fin.max()) if fin.size else -math.inf
+        if on_device:
+            fin = local[self.torch.isfinite(local)]
+            mx = float(fin.max().item()) if fin.numel() else -math.inf
+        else:
+            fin = local[np.isfinite(local)]
+            mx = float(fin.max()) if fin.size else -math.inf
         mx = self._allreduce(mx, R.MAX, self.torch.float64)
         outer = visited if skip_empty_buckets else bucket_index_of(mx, delta) + 1
         return ShardedResult(local, self.shard.v0, outer, phases, visited, exchanged, mode)
@@ -281,7 +300,7 @@ class PartitionedDeltaStepping:
     def _value(self, v: int, mode: int, frac: int) -> float:
         return math.ldexp(float(v), -frac) if mode == MODE_FIXED32 else _bits_f64(v)
 
-    def _run(self, source, delta, mode, frac, ceiling):
+    def _run(self, source, delta, mode, frac, ceiling, on_device=False):
         R = self.pg.ReduceOp
         torch = self.torch
         sh = self.shard
@@ -319,4 +338,5 @@ class PartitionedDeltaStepping:
             if self._allreduce(int(ovf), R.MAX, torch.int64):
                 return None
             idx += 1
-        return sh.result(), phases, visited, exchanged
+        local = sh.result(on_device=True) if on_device else sh.result()
+        return local, phases, visited, exchanged
