@@ -567,7 +567,7 @@ static int alloc_scratch(ds_graph* g) {
         CK(cudaMalloc(&pl->rowid, sizeof(int) * n));
         CK(cudaMalloc(&pl->cptr, sizeof(long long) * (n + 1)));
         CK(cudaMalloc(&pl->span, sizeof(int) * n));
-        CK(cudaMalloc(&pl->chunk_row, sizeof(unsigned) * (g->nnz / 256 + 4)));
+        CK(cudaMalloc(&pl->chunk_row, sizeof(unsigned) * (g->nnz / kChunk + 4)));
     }
     CK(cudaMalloc(&g->Rpre, sizeof(long long) * n));
     CK(cudaMalloc(&g->Rbase, sizeof(long long) * n));

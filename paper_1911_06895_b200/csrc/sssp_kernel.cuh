@@ -126,7 +126,10 @@ struct ModeF64 {
 constexpr int kPackShift = 33;  // capture reservation: (entries << 33) | edges
 constexpr unsigned long long kMask33 = (1ull << kPackShift) - 1;
 constexpr int kWarps = kThreads / 32;
-constexpr int kChunk = 256;       // relax / pull: edges per warp chunk (32 lanes x 8)
+#ifndef DS_CHUNK
+#define DS_CHUNK 256
+#endif
+constexpr int kChunk = DS_CHUNK;  // relax / pull: edges per warp chunk (32 lanes x kRelPer)
 constexpr int kRelPer = kChunk / 32;
 constexpr int kListPer = 4;       // capture (list): entries per lane
 constexpr int kRangePer = 16;     // capture (range): vertices per lane
@@ -595,8 +598,13 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
 // improvements that land inside the window join the next frontier once
 // (bitmap dedup); HEAVY: min-merge only (results land beyond the window).
 
+#ifndef DS_RELAX_INLINE
+#define DS_RELAX_INLINE __forceinline__
+#endif
+// Inlined: a __noinline__ push measured 25% slower (the kernel parameters
+// then live in a local-memory frame).
 template <class M, bool LIGHT>
-__device__ void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
+__device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                            unsigned long long E, unsigned long long Rc,
                            const typename M::Edge* edges, typename M::D H, int* out_list,
                            unsigned* fbits) {
