@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=("rmat", "grid", "er"), default="rmat",
+                    help="rmat: BASELINE configs 2/4/5 (--scale); grid: config 3 (4096^2, "
+                         "delta 25, source (0,0)); er: config 1 (n=1024, delta 3, source 0)")
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--delta", type=float, default=0.1)
@@ -350,14 +353,28 @@ def main():
     sptr = stream.cuda_stream
     delta = args.delta
 
-    # ---- graph: generated on the device, CSR mirrored in pinned host memory
-    g = DeviceGraph.rmat(args.scale, args.edge_factor, 1, 2, device=local, stream=sptr)
+    # ---- graph: generated on the device (R-MAT) or on the host (grid, ER);
+    # the CSR is mirrored in pinned host memory for the e2e leg
+    if args.config == "rmat":
+        g = DeviceGraph.rmat(args.scale, args.edge_factor, 1, 2, device=local, stream=sptr)
+        indptr_h, col_h, val_h = g.download()
+        pool = graphs.pick_sources(indptr_h, args.sources, seed=7)
+        workload = f"rmat{args.scale}_ef{args.edge_factor}_delta{delta}"
+    else:
+        if args.config == "grid":
+            h = graphs.grid2d(4096, seed=3)
+            delta = args.delta if args.delta != 0.1 else 25.0
+        else:
+            h = graphs.erdos_renyi(1024, seed=0)
+            delta = args.delta if args.delta != 0.1 else 3.0
+        indptr_h, col_h, val_h = h.indptr, h.col.astype(np.int32), h.val.astype(np.float32)
+        g = DeviceGraph.from_csr(h.n, indptr_h, col_h, val_h, device=local, stream=sptr)
+        pool = [0]
+        workload = f"{'grid4096' if args.config == 'grid' else 'er1024'}_delta{delta}_source0"
     n, nnz = g.n, g.nnz
-    indptr_h, col_h, val_h = g.download()
     pin_indptr = torch.from_numpy(indptr_h).pin_memory()
-    pin_col = torch.from_numpy(col_h).pin_memory()
-    pin_val = torch.from_numpy(val_h).pin_memory()
-    pool = graphs.pick_sources(indptr_h, args.sources, seed=7)
+    pin_col = torch.from_numpy(np.ascontiguousarray(col_h)).pin_memory()
+    pin_val = torch.from_numpy(np.ascontiguousarray(val_h)).pin_memory()
     # weak scaling: rank r takes sources r, r+ws, ... of the pool
     mine = pool[rank::ws] if ws > 1 else pool
 
@@ -501,7 +518,7 @@ def main():
             "dtype": "u32 fixed-point (exact f64)" if info.dist_mode == 0 else "f64",
             "data": "synthetic (seeded R-MAT, generated on device, fp32-lattice weights)",
             "config": {
-                "workload": f"rmat{args.scale}_ef{args.edge_factor}_delta{delta}",
+                "workload": workload,
                 "n": n, "nnz": nnz, "nnz_light": int(info.nnz_light),
                 "nnz_heavy": int(info.nnz_heavy), "sources_per_step": args.batch,
                 "source_pool": args.sources, "parallelism": f"replicas{ws}",

@@ -139,6 +139,7 @@ struct ds_graph {
     long long reached = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int grid_fixed = 0, grid_f64 = 0;
+    int occ_big_l = 1, occ_big_h = 1;
     size_t persist_bytes = 0, max_window = 0;
     unsigned long long* trace = nullptr;  // DS_TRACE=1: per-step timeline
     unsigned long long trace_cap = 0;
@@ -596,6 +597,18 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeF64>,
                                                      kThreads, sizeof(Smem<unsigned long long>)));
     g->grid_f64 = (int)grid_blocks_for(g->nsm, occ);
+    {   // standalone giant-push kernels (both modes share the block shape)
+        const int sf = (int)sizeof(Smem<unsigned>), s6 = (int)sizeof(Smem<unsigned long long>);
+        CK(cudaFuncSetAttribute(k_big_relax<ModeFixed, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sf));
+        CK(cudaFuncSetAttribute(k_big_relax<ModeFixed, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sf));
+        CK(cudaFuncSetAttribute(k_big_relax<ModeF64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s6));
+        CK(cudaFuncSetAttribute(k_big_relax<ModeF64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s6));
+        int o = 1;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_big_relax<ModeFixed, true>, kThreads, sf));
+        g->occ_big_l = std::max(o, 1);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_big_relax<ModeFixed, false>, kThreads, sf));
+        g->occ_big_h = std::max(o, 1);
+    }
     if (g->grid_fixed <= 0 || g->grid_f64 <= 0)
         return set_err(DS_ECUDA, "persistent solver kernel cannot be resident on this device");
     // L2 set-aside for the distance array (opt-in: DS_L2_PERSIST=1; measured
@@ -1005,6 +1018,10 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
         const char* b = getenv("DS_PULL_H");
         p.pull_light = a ? (float)atof(a) : 0.5f;
         p.pull_heavy = b ? (float)atof(b) : 4.0f;  // heavy pull measured slower: off
+        const char* bl = getenv("DS_BIG_L");
+        const char* bh = getenv("DS_BIG_H");
+        p.big_light = bl ? (unsigned long long)atoll(bl) : ~0ull;
+        p.big_heavy = bh ? (unsigned long long)atoll(bh) : (4ull << 20);
     }
     p.Rpre = g->Rpre;
     p.Rbase = g->Rbase;
@@ -1048,9 +1065,24 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     cfg.attrs = at;
     cfg.numAttrs = nattr;
     CK(cudaEventRecord(g->ev0, g->stream));
-    CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M>, p));
+    // The persistent kernel runs the whole solve on the device; it only stops
+    // to hand a giant push to k_big_relax (its own launch and register
+    // budget), after which it is relaunched and resumes from Ctl.
+    const size_t smem = sizeof(Smem<typename M::D>);
+    for (int hop = 0;; ++hop) {
+        CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M>, p));
+        CK(cudaMemcpyAsync(g->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
+        CK(cudaStreamSynchronize(g->stream));
+        const Ctl& h = *g->h_ctl;
+        if (h.abort || h.status != 0 || h.rs_req == 0) break;
+        const unsigned rgrid = (unsigned)(g->nsm * (h.rs_req == 1 ? g->occ_big_l : g->occ_big_h));
+        if (h.rs_req == 1)
+            k_big_relax<M, true><<<rgrid, kThreads, smem, g->stream>>>(p);
+        else
+            k_big_relax<M, false><<<rgrid, kThreads, smem, g->stream>>>(p);
+        CK(cudaGetLastError());
+    }
     CK(cudaEventRecord(g->ev1, g->stream));
-    CK(cudaMemcpyAsync(g->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
     CK(cudaStreamSynchronize(g->stream));
     const Ctl& c = *g->h_ctl;
     // an interrupted solve may leave dedup bits set: clear them for the next one

@@ -173,7 +173,17 @@ struct Ctl {
     unsigned long long phases, visited, edges_scanned, barriers, steps;
     long long last_bucket;
     unsigned long long pulls;  // light/heavy steps run as pulls
+    // resumable solver: the persistent kernel hands a giant push to a
+    // standalone launch (k_big_relax) and is relaunched where it left off
+    unsigned long long rs_pos, rs_req, rs_E, rs_Rc;
+    unsigned long long rs_st, rs_phases, rs_visited, rs_escanned, rs_nbar, rs_npull;
+    unsigned long long rs_re, rs_scount, rs_old_scount, rs_pp, rs_bpar;
+    long long rs_idx;
+    StepSlot xslot;  // results of the standalone push
 };
+
+enum : int { POS_FRESH = 0, POS_BUCKET = 1, POS_PHASE = 2, POS_AFTER_LIGHT = 3, POS_HEAVY = 4,
+             POS_AFTER_HEAVY = 5 };
 
 constexpr int kDevOverflow = 100;  // internal status: fixed-point overflow
 
@@ -199,6 +209,7 @@ struct KParams {
     int frac;
     int pull_enabled;
     float pull_light, pull_heavy;  // pull when push volume > frac * nnz
+    unsigned long long big_light, big_heavy;  // pushes with >= this many edges run standalone
     long long ceiling;
     unsigned long long timeout_ns;
     const long long* indptr;  // original CSR row offsets (for m_r)
@@ -888,14 +899,18 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     Ctl* const c = p.ctl;
     unsigned gen = 0;
     unsigned long long deadline = 0;
-    if (threadIdx.x == 0) deadline = globaltimer_ns() + p.timeout_ns;
+    const int pos0 = (int)ldcg(&c->rs_pos);
+    if (threadIdx.x == 0) {
+        deadline = globaltimer_ns() + p.timeout_ns;
+        gen = ldcg(&c->bar_gen);  // resumed launches continue the barrier sequence
+    }
 
     // ---- init: t = {source: 0} (sssp.py:276), all else +inf.  Only solver
     // ids below n_scan can ever be reached (the source may be an isolated
     // vertex outside the active prefix).
     const long long src = __ldg(p.perm + p.source);
     const long long n_scan = p.n_active > src + 1 ? p.n_active : src + 1;
-    {
+    if (pos0 == POS_FRESH) {
         const long long stride = (long long)gridDim.x * kThreads;
         for (long long v = (long long)blockIdx.x * kThreads + threadIdx.x; v < n_scan; v += stride)
             p.dist[v] = (v == src) ? (D)0 : M::INF;
@@ -908,15 +923,35 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             }
             c->s_count[0] = c->s_count[1] = 0;
         }
+        if (!grid_sync(c, gen, deadline, sm)) return;
+        if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) c->last_bucket = (long long)globaltimer_ns();
     }
-    if (!grid_sync(c, gen, deadline, sm)) return;
-    if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) c->last_bucket = (long long)globaltimer_ns();
 
-    unsigned long long st = 0;  // step counter (identical on every CTA)
-    unsigned long long nbar = 1, escanned = 0, npull = 0;
-    long long idx = 0;  // bucket index
+    // solver state (identical on every CTA; saved to / restored from Ctl)
+    unsigned long long st = 0, nbar = 1, escanned = 0, npull = 0;
+    long long idx = 0;
     unsigned long long phases = 0, visited = 0;
+    unsigned long long re = 0, scount = 0, old_scount = 0;
     int pp = 0;
+    unsigned bpar = 0;
+    int pos = POS_BUCKET;
+    bool resumed = false;
+    if (pos0 != POS_FRESH) {
+        st = ldcg(&c->rs_st);
+        nbar = ldcg(&c->rs_nbar);
+        escanned = ldcg(&c->rs_escanned);
+        npull = ldcg(&c->rs_npull);
+        idx = ldcg(&c->rs_idx);
+        phases = ldcg(&c->rs_phases);
+        visited = ldcg(&c->rs_visited);
+        re = ldcg(&c->rs_re);
+        scount = ldcg(&c->rs_scount);
+        old_scount = ldcg(&c->rs_old_scount);
+        pp = (int)ldcg(&c->rs_pp);
+        bpar = (unsigned)ldcg(&c->rs_bpar);
+        pos = pos0;
+        resumed = true;
+    }
     int status = 0;
 
     auto end_step = [&](unsigned long long kind, unsigned long long work) -> bool {
@@ -936,12 +971,37 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         return ok;
     };
     auto prev = [&]() -> StepSlot* { return &c->slot[(st + 2) % 3]; };
-    unsigned bpar = 0;                  // S list / counter parity (flips per visited bucket)
-    unsigned long long old_scount = 0;  // previous bucket's S, retired by the next scan
+    // hand a giant push to the host-launched standalone kernel and stop
+    auto handoff = [&](int next_pos, unsigned long long req, unsigned long long E,
+                       unsigned long long Rc) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            c->rs_pos = (unsigned long long)next_pos;
+            c->rs_req = req;
+            c->rs_E = E;
+            c->rs_Rc = Rc;
+            c->rs_st = st;
+            c->rs_nbar = nbar;
+            c->rs_escanned = escanned + E;
+            c->rs_npull = npull;
+            c->rs_idx = idx;
+            c->rs_phases = phases;
+            c->rs_visited = visited;
+            c->rs_re = re;
+            c->rs_scount = scount;
+            c->rs_old_scount = old_scount;
+            c->rs_pp = (unsigned long long)pp;
+            c->rs_bpar = bpar;
+            StepSlot* x = &c->xslot;
+            x->re_packed = x->front_count = x->append_count = 0;
+            x->flags = 0;
+            x->next_min = ~0ull;
+        }
+    };
     const unsigned long long pullL =
         p.pull_enabled ? (unsigned long long)(p.pull_light * (float)p.Lpull.nnz) : ~0ull;
     const unsigned long long pullH =
         p.pull_enabled ? (unsigned long long)(p.pull_heavy * (float)p.Hpull.nnz) : ~0ull;
+    unsigned long long nf = 0;
 
     for (;;) {
         const double lo = (double)idx * p.delta;
@@ -949,33 +1009,38 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         D L, H;
         M::window(lo, hi, p.frac, L, H);
 
-        // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
-        if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[bpar ^ 1] = 0;
-        capture_range<M>(p, sm, &c->slot[st % 3], L, H, p.S[bpar], &c->s_count[bpar],
-                         (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount);
-        old_scount = 0;
-        if (!end_step(0, (unsigned long long)n_scan)) return;
-        const unsigned long long fc = ldcg(&prev()->front_count);
-        unsigned long long re = ldcg(&prev()->re_packed);
-        if (fc == 0) {
-            const unsigned long long nm = ldcg(&prev()->next_min);
-            if (nm == ~0ull) break;  // nothing stored beyond: done
-            idx = bucket_index_of(M::to_f64((D)nm, p.frac), p.delta);
-            continue;
+        if (pos == POS_BUCKET) {
+            // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
+            if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[bpar ^ 1] = 0;
+            capture_range<M>(p, sm, &c->slot[st % 3], L, H, p.S[bpar], &c->s_count[bpar],
+                             (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount);
+            old_scount = 0;
+            if (!end_step(0, (unsigned long long)n_scan)) return;
+            const unsigned long long fc = ldcg(&prev()->front_count);
+            re = ldcg(&prev()->re_packed);
+            if (fc == 0) {
+                const unsigned long long nm = ldcg(&prev()->next_min);
+                if (nm == ~0ull) break;  // nothing stored beyond: done
+                idx = bucket_index_of(M::to_f64((D)nm, p.frac), p.delta);
+                continue;
+            }
+            ++visited;
+            pos = POS_PHASE;
         }
-        ++visited;
 
-        // ---- light phases (sssp.py:292-301)
-        for (;;) {
+        if (pos == POS_PHASE) {
+            // ---- one light phase (sssp.py:292-301)
             ++phases;
             if ((long long)phases > p.ceiling) {
                 status = 2;  // DS_ENOCONVERGE
                 break;
             }
-            unsigned long long nf = 0;
-            bool vals = false;
+            nf = 0;
             const unsigned long long E = re & kMask33;
-            unsigned* fb = p.fbits[phases & 1];
+            if (E >= p.big_light) {
+                handoff(POS_AFTER_LIGHT, 1, E, re >> kPackShift);
+                return;
+            }
             if (DS_PULL_LIGHT && E > pullL) {
                 escanned += (unsigned long long)p.Lpull.nnz;
                 ++npull;
@@ -990,11 +1055,21 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                     break;
                 }
                 nf = ldcg(&c->slot[sl].append_count);
-                vals = true;
+                // values travel with the list; commit them in the next capture
+                capture_list<M, true, true>(p, sm, &c->slot[st % 3], p.F[pp], p.Fv[pp], nf, p.Lptr,
+                                            p.fbits[phases & 1], p.S[bpar], &c->s_count[bpar]);
+                if (nf == 0) {
+                    pos = POS_HEAVY;
+                    continue;
+                }
+                if (!end_step(2, nf)) return;
+                re = ldcg(&prev()->re_packed);
+                pp ^= 1;
+                continue;
             } else if (E > 0) {
                 escanned += E;
                 relax_step<M, true>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Ledges, H,
-                                    p.F[pp], fb);
+                                    p.F[pp], p.fbits[phases & 1]);
                 if (!end_step(1, E)) return;
                 if (ldcg(&prev()->flags) & 1u) {
                     status = kDevOverflow;
@@ -1002,52 +1077,81 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 }
                 nf = ldcg(&prev()->append_count);
             }
-            if (nf == 0) break;
-            if (vals)
-                capture_list<M, true, true>(p, sm, &c->slot[st % 3], p.F[pp], p.Fv[pp], nf, p.Lptr,
-                                            fb, p.S[bpar], &c->s_count[bpar]);
-            else
-                capture_list<M, true, false>(p, sm, &c->slot[st % 3], p.F[pp], nullptr, nf, p.Lptr,
-                                             fb, p.S[bpar], &c->s_count[bpar]);
-            if (!end_step(2, nf)) return;
-            re = ldcg(&prev()->re_packed);
-            pp ^= 1;
+            pos = POS_AFTER_LIGHT;
+        } else if (pos == POS_AFTER_LIGHT && resumed) {
+            // results of the standalone light push
+            resumed = false;
+            if (ldcg(&c->xslot.flags) & 1u) {
+                status = kDevOverflow;
+                break;
+            }
+            nf = ldcg(&c->xslot.append_count);
         }
-        if (status) break;
 
-        // ---- heavy relaxation from S with current t (sssp.py:218-227)
-        const unsigned long long scount = ldcg(&c->s_count[bpar]);
-        capture_list<M, false, false>(p, sm, &c->slot[st % 3], p.S[bpar], nullptr, scount, p.Hptr,
-                                      nullptr, nullptr, nullptr);
-        if (!end_step(3, scount)) return;
-        re = ldcg(&prev()->re_packed);
-        const unsigned long long E = re & kMask33;
-        if (DS_PULL_HEAVY && E > pullH) {
-            escanned += (unsigned long long)p.Hpull.nnz;
-            ++npull;
-            const unsigned sl = (unsigned)(st % 3);
-            pull_step<M, false>(p, sm, &c->slot[sl], p.Hpull, p.Hedges, L, H, nullptr, nullptr);
-            if (!end_step(7, (unsigned long long)p.Hpull.nnz)) return;
-            const bool ovf = ldcg(&prev()->flags) & 1u;
-            commit_step<M, false>(p, sm, &c->slot[sl], p.Hpull, H, nullptr, nullptr);
-            if (!end_step(8, (unsigned long long)p.Hpull.nspan)) return;
-            if (ovf) {
-                status = kDevOverflow;
-                break;
+        if (pos == POS_AFTER_LIGHT) {
+            if (nf == 0) {
+                pos = POS_HEAVY;
+            } else {
+                capture_list<M, true, false>(p, sm, &c->slot[st % 3], p.F[pp], nullptr, nf, p.Lptr,
+                                             p.fbits[phases & 1], p.S[bpar], &c->s_count[bpar]);
+                if (!end_step(2, nf)) return;
+                re = ldcg(&prev()->re_packed);
+                pp ^= 1;
+                pos = POS_PHASE;
+                continue;
             }
-        } else if (E > 0) {
-            escanned += E;
-            relax_step<M, false>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Hedges, H,
-                                 nullptr, nullptr);
-            if (!end_step(4, E)) return;
-            if (ldcg(&prev()->flags) & 1u) {
+        }
+
+        if (pos == POS_HEAVY) {
+            // ---- heavy relaxation from S with current t (sssp.py:218-227)
+            scount = ldcg(&c->s_count[bpar]);
+            capture_list<M, false, false>(p, sm, &c->slot[st % 3], p.S[bpar], nullptr, scount,
+                                          p.Hptr, nullptr, nullptr, nullptr);
+            if (!end_step(3, scount)) return;
+            re = ldcg(&prev()->re_packed);
+            const unsigned long long E = re & kMask33;
+            if (E >= p.big_heavy) {
+                handoff(POS_AFTER_HEAVY, 2, E, re >> kPackShift);
+                return;
+            }
+            if (DS_PULL_HEAVY && E > pullH) {
+                escanned += (unsigned long long)p.Hpull.nnz;
+                ++npull;
+                const unsigned sl = (unsigned)(st % 3);
+                pull_step<M, false>(p, sm, &c->slot[sl], p.Hpull, p.Hedges, L, H, nullptr, nullptr);
+                if (!end_step(7, (unsigned long long)p.Hpull.nnz)) return;
+                const bool ovf = ldcg(&prev()->flags) & 1u;
+                commit_step<M, false>(p, sm, &c->slot[sl], p.Hpull, H, nullptr, nullptr);
+                if (!end_step(8, (unsigned long long)p.Hpull.nspan)) return;
+                if (ovf) {
+                    status = kDevOverflow;
+                    break;
+                }
+            } else if (E > 0) {
+                escanned += E;
+                relax_step<M, false>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Hedges, H,
+                                     nullptr, nullptr);
+                if (!end_step(4, E)) return;
+                if (ldcg(&prev()->flags) & 1u) {
+                    status = kDevOverflow;
+                    break;
+                }
+            }
+            pos = POS_AFTER_HEAVY;
+        } else if (pos == POS_AFTER_HEAVY && resumed) {
+            resumed = false;
+            if (ldcg(&c->xslot.flags) & 1u) {
                 status = kDevOverflow;
                 break;
             }
         }
-        old_scount = scount;
-        bpar ^= 1;
-        ++idx;
+
+        if (pos == POS_AFTER_HEAVY) {
+            old_scount = scount;
+            bpar ^= 1;
+            ++idx;
+            pos = POS_BUCKET;
+        }
     }
 
     if (status) {
@@ -1055,6 +1159,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             c->status = status;
             c->phases = phases;
             c->steps = st;
+            c->rs_req = 0;
         }
         return;
     }
@@ -1093,11 +1198,36 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 c->barriers = nbar;
                 c->steps = st;
                 c->pulls = npull;
+                c->rs_req = 0;
                 if (!p.trace) c->last_bucket = idx;
                 c->status = 0;
             }
         }
     }
+}
+
+// A giant push handed off by the persistent kernel, as its own launch (its
+// own register allocation, no spills): the solver state says which list,
+// window and CSR; results land in Ctl::xslot.
+template <class M, bool LIGHT>
+__global__ void __launch_bounds__(kThreads) k_big_relax(const KParams<M> p) {
+    using D = typename M::D;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
+    Ctl* const c = p.ctl;
+    const long long idx = ldcg(&c->rs_idx);
+    const double lo = (double)idx * p.delta;
+    const double hi = (double)(idx + 1) * p.delta;
+    D L, H;
+    M::window(lo, hi, p.frac, L, H);
+    const unsigned long long E = ldcg(&c->rs_E), Rc = ldcg(&c->rs_Rc);
+    const int pp = (int)ldcg(&c->rs_pp);
+    const unsigned long long phases = ldcg(&c->rs_phases);
+    if (LIGHT)
+        relax_step<M, true>(p, sm, &c->xslot, E, Rc, p.Ledges, H, p.F[pp], p.fbits[phases & 1]);
+    else
+        relax_step<M, false>(p, sm, &c->xslot, E, Rc, p.Hedges, H, nullptr, nullptr);
+    (void)L;
 }
 
 }  // namespace ds

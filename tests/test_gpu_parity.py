@@ -284,3 +284,41 @@ def test_pull_variant_exact_on_symmetric_graphs():
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "pull ok" in r.stdout
+
+
+_HANDOFF_SCRIPT = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["REPO"])
+import oracle
+from paper_1911_06895_b200 import DeviceGraph, graphs
+cases = [(graphs.rmat(16, seed=3, weight_seed=4), 0.1), (graphs.grid2d(64, seed=3), 25.0),
+         (graphs.erdos_renyi(1024, seed=0), 3.0)]
+for a, d in cases:
+    g = DeviceGraph.from_matrix(a)
+    for s in graphs.pick_sources(a.indptr, 2, seed=5):
+        st = g.solve(s, d)
+        got = g.result_dense()
+        want, outer, phases = oracle.delta_stepping(a.n, a.indptr, a.col, a.val, s, d, threads=4)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (a.n, s)
+        assert (st.inner_phases, st.outer_iterations) == (phases, outer)
+        st64 = g.solve(s, d, force_f64=True)
+        assert np.array_equal(g.result_dense().view(np.uint64), want.view(np.uint64))
+    g.close()
+print("handoff ok")
+"""
+
+
+def test_giant_push_handoff_is_exact():
+    """Every push handed to the standalone k_big_relax launch (thresholds
+    forced down): the resumed persistent kernel stays bit-exact."""
+    import os
+    import subprocess
+    import sys
+
+    from paper_1911_06895_b200.build import REPO
+
+    env = dict(os.environ, DS_BIG_L="64", DS_BIG_H="64", REPO=REPO)
+    r = subprocess.run([sys.executable, "-c", _HANDOFF_SCRIPT], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "handoff ok" in r.stdout
