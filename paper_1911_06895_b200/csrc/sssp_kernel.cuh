@@ -683,23 +683,36 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                 }
             }
         }
+        if (LIGHT) {
+            // all pushes first, then all dedup claims, then the appends: the
+            // returning atomics of one chunk overlap instead of serialising
+            // behind a warp vote per edge
+            D old[kRelPer];
 #pragma unroll
-        for (int j = 0; j < kRelPer; ++j) {
-            const bool go = 32 * j < left && nd[j] < cur[j];
-            const unsigned v = go ? M::col(ed[j]) : 0u;
-            if (LIGHT) {
-                bool want = false;
-                if (go) {
-                    const D old = atomicMin(p.dist + v, nd[j]);
-                    want = nd[j] < old && nd[j] < H && claim_bit(fbits, v);
-                }
-                wq_push<D, false>(ws.q, ws.qv, qn, want, (int)v, (D)0, lane, out_list, nullptr,
-                                  &slot->append_count);
-            } else if (go) {
-                atomicMin(p.dist + v, nd[j]);
+            for (int j = 0; j < kRelPer; ++j) {
+                old[j] = nd[j];
+                if (32 * j < left && nd[j] < cur[j]) old[j] = atomicMin(p.dist + M::col(ed[j]), nd[j]);
             }
+            unsigned got[kRelPer];
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                got[j] = 0;
+                if (32 * j < left && nd[j] < old[j] && nd[j] < H) {
+                    const unsigned v = M::col(ed[j]);
+                    got[j] = atomicOr(fbits + (v >> 5), 1u << (v & 31)) & (1u << (v & 31));
+                    got[j] = got[j] ? 0u : 1u;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j)
+                wq_push<D, false>(ws.q, ws.qv, qn, got[j] != 0, (int)M::col(ed[j]), (D)0, lane,
+                                  out_list, nullptr, &slot->append_count);
+            wq_flush<D, false>(ws.q, ws.qv, qn, lane, out_list, nullptr, &slot->append_count);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j)
+                if (32 * j < left && nd[j] < cur[j]) atomicMin(p.dist + M::col(ed[j]), nd[j]);
         }
-        if (LIGHT) wq_flush<D, false>(ws.q, ws.qv, qn, lane, out_list, nullptr, &slot->append_count);
         __syncwarp();
     }
     if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, 1u);
