@@ -529,6 +529,7 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
                     cd[j] = dv[b];
                 }
             }
+            bool news[kListPer];
 #pragma unroll
             for (int j = 0; j < kListPer; ++j) {
                 const bool in = vtx[j] >= 0;
@@ -536,9 +537,11 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
                     off[j] = __ldg(p.Lptr + vtx[j]);
                     deg[j] = __ldg(p.Lptr + vtx[j] + 1) - off[j];
                 }
-                const bool news = in && claim_bit(p.sbits, (unsigned)vtx[j]);
-                wq_push<D, false>(ws.q, ws.qv, qn, news, vtx[j], (D)0, lane, S, nullptr, s_counter);
+                news[j] = in && claim_bit(p.sbits, (unsigned)vtx[j]);
             }
+#pragma unroll
+            for (int j = 0; j < kListPer; ++j)
+                wq_push<D, false>(ws.q, ws.qv, qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
             capture_emit<M, kListPer>(p, slot, lane, cd, off, deg);
         }
         wq_flush<D, false>(ws.q, ws.qv, qn, lane, S, nullptr, s_counter);
@@ -592,11 +595,12 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
             if (in[j] && clear_bits) clear_bits[(unsigned)vtx[j] >> 5] = 0u;
         }
         if (APPEND_S) {
+            bool news[kListPer];
 #pragma unroll
-            for (int j = 0; j < kListPer; ++j) {
-                const bool news = in[j] && claim_bit(p.sbits, (unsigned)vtx[j]);
-                wq_push<D, false>(ws.q, ws.qv, qn, news, vtx[j], (D)0, lane, S, nullptr, s_counter);
-            }
+            for (int j = 0; j < kListPer; ++j) news[j] = in[j] && claim_bit(p.sbits, (unsigned)vtx[j]);
+#pragma unroll
+            for (int j = 0; j < kListPer; ++j)
+                wq_push<D, false>(ws.q, ws.qv, qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
             wq_flush<D, false>(ws.q, ws.qv, qn, lane, S, nullptr, s_counter);
         }
         capture_emit<M, kListPer>(p, slot, lane, dv, off, deg);
