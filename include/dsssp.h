@@ -122,6 +122,9 @@ int ds_graph_set_stream(ds_graph* g, void* stream);
 int ds_graph_size(const ds_graph* g, int64_t* n, int64_t* nnz);
 
 void ds_graph_destroy(ds_graph* g);
+/* Graph buffers are pooled per device and reused by later handles; this
+ * returns every cached buffer to the driver. */
+void ds_release_pool(void);
 const char* ds_last_error(void);
 int ds_device_count(void);
 

@@ -25,6 +25,7 @@ EXPORTS = (
     "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download", "ds_debug_trace",
     "ds_shard_create", "ds_shard_destroy", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",
     "ds_shard_scan", "ds_shard_s_add", "ds_shard_relax", "ds_shard_result", "ds_shard_from_graph",
+    "ds_release_pool",
 )
 
 
@@ -100,6 +101,8 @@ def lib():
         L.ds_graph_size.argtypes = [_vp, _i64p, _i64p]
         L.ds_graph_destroy.argtypes = [_vp]
         L.ds_graph_destroy.restype = None
+        L.ds_release_pool.argtypes = []
+        L.ds_release_pool.restype = None
         L.ds_last_error.restype = ctypes.c_char_p
         L.ds_device_count.restype = ctypes.c_int
         L.ds_gen_rmat.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64,

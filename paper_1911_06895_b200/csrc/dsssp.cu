@@ -27,6 +27,93 @@
 
 using namespace ds;
 
+// ---------------------------------------------------------------- buffer pool
+//
+// Graph handles allocate O(n + nnz) device buffers; cudaMalloc / cudaFree of
+// many GB costs hundreds of ms (measured on the e2e path).  Freed buffers are
+// kept per device and size and reused by the next handle (DS_POOL=0 disables;
+// ds_release_pool() returns them to the driver; an allocation failure releases
+// the cache and retries).
+#include <map>
+#include <mutex>
+#include <unordered_map>
+
+namespace {
+struct BufferPool {
+    std::mutex m;
+    std::multimap<std::pair<int, size_t>, void*> free_;
+    std::unordered_map<void*, std::pair<int, size_t>> live_;
+};
+BufferPool& buffer_pool() {
+    static BufferPool* p = new BufferPool();  // never destroyed: safe at process exit
+    return *p;
+}
+bool pool_on() {
+    static const bool on = [] {
+        const char* s = getenv("DS_POOL");
+        return !(s && atoi(s) == 0);
+    }();
+    return on;
+}
+void pool_release_locked(BufferPool& P) {
+    for (auto& kv : P.free_) {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(kv.first.first);
+        cudaFree(kv.second);
+        cudaSetDevice(cur);
+    }
+    P.free_.clear();
+}
+}  // namespace
+
+static cudaError_t ds_pool_malloc(void** ptr, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    BufferPool& P = buffer_pool();
+    std::lock_guard<std::mutex> lk(P.m);
+    if (pool_on()) {
+        auto it = P.free_.lower_bound({dev, bytes});
+        if (it != P.free_.end() && it->first.first == dev && it->first.second <= bytes + bytes / 2 + (1u << 20)) {
+            *ptr = it->second;
+            P.live_[*ptr] = it->first;
+            P.free_.erase(it);
+            return cudaSuccess;
+        }
+    }
+    cudaError_t e = cudaMalloc(ptr, bytes);
+    if (e == cudaErrorMemoryAllocation && !P.free_.empty()) {
+        cudaGetLastError();
+        pool_release_locked(P);
+        e = cudaMalloc(ptr, bytes);
+    }
+    if (e == cudaSuccess) P.live_[*ptr] = {dev, bytes};
+    return e;
+}
+
+static cudaError_t ds_pool_free(void* ptr) {
+    if (!ptr) return cudaSuccess;
+    BufferPool& P = buffer_pool();
+    std::lock_guard<std::mutex> lk(P.m);
+    auto it = P.live_.find(ptr);
+    if (it == P.live_.end()) return cudaFree(ptr);
+    const auto key = it->second;
+    P.live_.erase(it);
+    if (!pool_on()) return cudaFree(ptr);
+    P.free_.insert({key, ptr});
+    return cudaSuccess;
+}
+
+extern "C" void ds_release_pool(void) {
+    BufferPool& P = buffer_pool();
+    std::lock_guard<std::mutex> lk(P.m);
+    pool_release_locked(P);
+}
+
+#define cudaMalloc(pp, bytes) ds_pool_malloc((void**)(pp), (bytes))
+#define cudaFree(p) ds_pool_free((void*)(p))
+
 // ---------------------------------------------------------------- errors
 
 static thread_local std::string g_err;
@@ -126,7 +213,7 @@ struct ds_graph {
     int* perm = nullptr;   // input id -> solver id
     long long n_active = 0;
     Ctl* ctl = nullptr;
-    Ctl* h_ctl = nullptr;  // pinned
+    Ctl* h_ctl = nullptr;  // host mirror
     PrepStats* pstat = nullptr;
     PrepStats* h_pstat = nullptr;
     double* out = nullptr;
@@ -156,8 +243,8 @@ static void free_all(ds_graph* g) {
                     g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    if (g->h_ctl) cudaFreeHost(g->h_ctl);
-    if (g->h_pstat) cudaFreeHost(g->h_pstat);
+    delete g->h_ctl;  // small pageable mirrors (cudaFreeHost costs ms per call)
+    delete g->h_pstat;
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
 }
@@ -561,6 +648,7 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaMalloc(&g->F1, sizeof(int) * n));
     CK(cudaMalloc(&g->S0, sizeof(int) * n));
     CK(cudaMalloc(&g->S1, sizeof(int) * n));
+    if (DS_PULL_LIGHT || DS_PULL_HEAVY) {  // pull-only state
     CK(cudaMalloc(&g->Fv0, sizeof(unsigned long long) * n));
     CK(cudaMalloc(&g->Fv1, sizeof(unsigned long long) * n));
     CK(cudaMalloc(&g->req, sizeof(unsigned long long) * n));
@@ -570,14 +658,15 @@ static int alloc_scratch(ds_graph* g) {
         CK(cudaMalloc(&pl->span, sizeof(int) * n));
         CK(cudaMalloc(&pl->chunk_row, sizeof(unsigned) * (g->nnz / kChunk + 4)));
     }
+    }
     CK(cudaMalloc(&g->Rpre, sizeof(long long) * n));
     CK(cudaMalloc(&g->Rbase, sizeof(long long) * n));
     CK(cudaMalloc(&g->Rd, sizeof(unsigned long long) * n));
     CK(cudaMalloc(&g->chunk_start, sizeof(unsigned) * (g->nnz / kChunk + 4)));
     CK(cudaMalloc(&g->ctl, sizeof(Ctl)));
-    CK(cudaMallocHost(&g->h_ctl, sizeof(Ctl)));
+    g->h_ctl = new Ctl();
     CK(cudaMalloc(&g->pstat, sizeof(PrepStats)));
-    CK(cudaMallocHost(&g->h_pstat, sizeof(PrepStats)));
+    g->h_pstat = new PrepStats();
     CK(cudaMalloc(&g->out, sizeof(double) * n));
     CK(cudaMalloc(&g->Lptr, sizeof(long long) * (n + 1)));
     CK(cudaMalloc(&g->Hptr, sizeof(long long) * (n + 1)));
@@ -943,13 +1032,13 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
                                                               (EdgeF64*)g->Ledges,
                                                               (EdgeF64*)g->Hedges);
     CK(cudaGetLastError());
-    if (g->symmetric) {  // pull schedules (A^T == A: rows serve as columns)
+    if (g->symmetric && (DS_PULL_LIGHT || DS_PULL_HEAVY)) {  // pull schedules (A^T == A)
         if ((rc = build_plan(g, g->Lptr, g->nL, g->planL))) return rc;
         if ((rc = build_plan(g, g->Hptr, g->nH, g->planH))) return rc;
     }
-    if (mode == DS_MODE_FIXED32)
+    if (g->req && mode == DS_MODE_FIXED32)
         k_fill<unsigned><<<elementwise_grid(g), 256, 0, g->stream>>>((unsigned*)g->req, g->n, ModeFixed::INF);
-    else
+    else if (g->req)
         k_fill<unsigned long long><<<elementwise_grid(g), 256, 0, g->stream>>>(
             (unsigned long long*)g->req, g->n, ModeF64::INF);
     CK(cudaGetLastError());
