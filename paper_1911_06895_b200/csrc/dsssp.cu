@@ -316,18 +316,19 @@ __device__ __forceinline__ bool light_w(double w, double delta) { return w > 0.0
 __device__ __forceinline__ bool heavy_w(double w, double delta) { return w > delta && w < CUDART_INF; }
 
 // warp per row: light/heavy counts, min light weight, fixed-point eligibility
-// Rows are visited in solver order: row r of the output is input row
-// order[r] (identity when order == nullptr), columns are renamed through perm.
+// Input rows are read in input order (sequential, coalesced); input row v
+// becomes output row perm[v] (identity when perm == nullptr) and columns are
+// renamed through perm -- the solver's degree-sorted relabeling.
 __global__ void k_split_count(long long n, const long long* indptr, const double* w, double delta,
-                              const int* order, long long* Lcnt, long long* Hcnt, PrepStats* st) {
+                              const int* perm, long long* Lcnt, long long* Hcnt, PrepStats* st) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     unsigned long long minL = ~0ull, maxw = 0, nl = 0, nh = 0;
     int frac = 0;
-    for (long long r = warp; r < n; r += nwarps) {
-        const long long o = order ? order[r] : r;
-        const long long a = indptr[o], b = indptr[o + 1];
+    for (long long v = warp; v < n; v += nwarps) {
+        const long long a = indptr[v], b = indptr[v + 1];
+        const long long r = perm ? perm[v] : v;
         unsigned lc = 0, hc = 0;
         for (long long e = a + lane; e < b; e += 32) {
             const double x = __ldg(w + e);
@@ -383,16 +384,16 @@ __device__ __forceinline__ void put_edge(EdgeF64* out, long long i, int c, doubl
 // filter_matrix semantics, ops.py:158-176)
 template <class Edge>
 __global__ void k_split_scatter(long long n, const long long* indptr, const int* col,
-                                const double* w, double delta, int frac, const int* order,
-                                const int* perm, const long long* Lptr, const long long* Hptr,
-                                Edge* Lout, Edge* Hout) {
+                                const double* w, double delta, int frac, const int* perm,
+                                const long long* Lptr, const long long* Hptr, Edge* Lout,
+                                Edge* Hout) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    for (long long r = warp; r < n; r += nwarps) {
-        const long long o = order ? order[r] : r;
-        const long long a = indptr[o], b = indptr[o + 1];
+    for (long long v = warp; v < n; v += nwarps) {
+        const long long a = indptr[v], b = indptr[v + 1];
+        const long long r = perm ? perm[v] : v;
         long long lb = Lptr[r], hb = Hptr[r];
         for (long long e0 = a; e0 < b; e0 += 32) {
             const long long e = e0 + lane;
@@ -942,7 +943,7 @@ extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, co
     CKG(cudaStreamSynchronize(g->stream));
     if (h & 2) return fail(set_err(DS_EINVAL, "column index out of range for dimension %lld", (long long)n));
     if ((rc = compute_order(g))) return fail(rc);
-    if ((rc = check_symmetric(g))) return fail(rc);
+    if ((DS_PULL_LIGHT || DS_PULL_HEAVY) && (rc = check_symmetric(g))) return fail(rc);
 #undef CKG
     *out = g;
     return DS_OK;
@@ -984,7 +985,7 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     CK(cudaMemsetAsync(g->Hptr, 0, sizeof(long long), g->stream));
     // per-row counts into scratch (Rpre / Rbase are n-sized int64)
     const unsigned grid = (unsigned)(g->nsm * 16);
-    k_split_count<<<grid, 256, 0, g->stream>>>(n, g->indptr, g->w, delta, g->order, g->Rpre, g->Rbase,
+    k_split_count<<<grid, 256, 0, g->stream>>>(n, g->indptr, g->w, delta, g->perm, g->Rpre, g->Rbase,
                                                g->pstat);
     CK(cudaGetLastError());
     int rc = inclusive_scan_i64(g, g->Rpre, g->Lptr + 1, n);
@@ -1024,11 +1025,11 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     if ((rc = ensure_edges(&g->Hedges, &g->Hcap, esz * (size_t)g->nH))) return rc;
     if (mode == DS_MODE_FIXED32)
         k_split_scatter<uint2><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, delta, g->frac,
-                                                            g->order, g->perm, g->Lptr, g->Hptr,
+                                                            g->perm, g->Lptr, g->Hptr,
                                                             (uint2*)g->Ledges, (uint2*)g->Hedges);
     else
         k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, delta, 0,
-                                                              g->order, g->perm, g->Lptr, g->Hptr,
+                                                              g->perm, g->Lptr, g->Hptr,
                                                               (EdgeF64*)g->Ledges,
                                                               (EdgeF64*)g->Hedges);
     CK(cudaGetLastError());
@@ -1348,7 +1349,7 @@ extern "C" int ds_export_split(ds_graph* g, int which, int64_t* indptr, int64_t*
     if ((rc = inclusive_scan_i64(g, g->Rpre, ptrL + 1, n))) return done(rc);
     if ((rc = inclusive_scan_i64(g, g->Rbase, ptrH + 1, n))) return done(rc);
     k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, g->delta, 0,
-                                                          nullptr, nullptr, ptrL, ptrH, eL, eH);
+                                                          nullptr, ptrL, ptrH, eL, eH);
     CKE(cudaGetLastError());
     CKE(cudaMemcpyAsync(indptr, which ? ptrH : ptrL, sizeof(long long) * (n + 1), cudaMemcpyDefault,
                         g->stream));
@@ -1412,7 +1413,7 @@ int ds_internal_adopt(ds_graph** out, int device, void* stream, long long n, lon
     g->w = w;
     int rc = alloc_scratch(g);
     if (!rc) rc = compute_order(g);
-    if (!rc) rc = check_symmetric(g);
+    if (!rc && (DS_PULL_LIGHT || DS_PULL_HEAVY)) rc = check_symmetric(g);
     if (rc) {
         free_all(g);
         delete g;
