@@ -227,6 +227,7 @@ struct ds_graph {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int grid_fixed = 0, grid_f64 = 0;
     int occ_big_l = 1, occ_big_h = 1;
+    bool small = false;  // use the block-local-phase kernel (high-diameter graphs)
     size_t persist_bytes = 0, max_window = 0;
     unsigned long long* trace = nullptr;  // DS_TRACE=1: per-step timeline
     unsigned long long trace_cap = 0;
@@ -675,18 +676,26 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaMemsetAsync(g->sbits, 0, sizeof(unsigned) * g->nwords, g->stream));
     CK(cudaEventCreate(&g->ev0));
     CK(cudaEventCreate(&g->ev1));
-    int occ = 0;
-    CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeFixed>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<unsigned>)));
-    CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeF64>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)sizeof(Smem<unsigned long long>)));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeFixed>,
-                                                     kThreads, sizeof(Smem<unsigned>)));
-    g->grid_fixed = (int)grid_blocks_for(g->nsm, occ);
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeF64>,
-                                                     kThreads, sizeof(Smem<unsigned long long>)));
-    g->grid_f64 = (int)grid_blocks_for(g->nsm, occ);
+    int occ = 0, occ2 = 0;
+    const int smf = (int)sizeof(Smem<unsigned>), sm6 = (int)sizeof(Smem<unsigned long long>);
+    CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeFixed, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, smf));
+    CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeFixed, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, smf));
+    CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeF64, false>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm6));
+    CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeF64, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, sm6));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeFixed, false>,
+                                                     kThreads, smf));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, sssp_persistent_kernel<ModeFixed, true>,
+                                                     kThreads, smf));
+    g->grid_fixed = (int)grid_blocks_for(g->nsm, std::min(occ, occ2));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeF64, false>,
+                                                     kThreads, sm6));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, sssp_persistent_kernel<ModeF64, true>,
+                                                     kThreads, sm6));
+    g->grid_f64 = (int)grid_blocks_for(g->nsm, std::min(occ, occ2));
     {   // standalone giant-push kernels (both modes share the block shape)
         const int sf = (int)sizeof(Smem<unsigned>), s6 = (int)sizeof(Smem<unsigned long long>);
         CK(cudaFuncSetAttribute(k_big_relax<ModeFixed, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sf));
@@ -790,6 +799,20 @@ static int check_symmetric(ds_graph* g) {
     CK(cudaStreamSynchronize(g->stream));
     g->symmetric = (h[0] == h[2] && h[1] == h[3]);
     return DS_OK;
+}
+
+// Low-degree graphs (grids, meshes, road networks) have high diameter and
+// tiny frontiers: thousands of buckets whose phases are latency-bound, so
+// they run the kernel whose small phases stay on one CTA (block barriers
+// instead of grid barriers).  DS_SMALL=0/1 overrides.
+static void choose_kernel(ds_graph* g) {
+    const char* e = getenv("DS_SMALL");
+    if (e) {
+        g->small = atoi(e) != 0;
+        return;
+    }
+    const double deg = g->n_active > 0 ? (double)g->nnz / (double)g->n_active : 0.0;
+    g->small = deg > 0.0 && deg < 6.0;
 }
 
 static int compute_order(ds_graph* g) {
@@ -943,6 +966,7 @@ extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, co
     CKG(cudaStreamSynchronize(g->stream));
     if (h & 2) return fail(set_err(DS_EINVAL, "column index out of range for dimension %lld", (long long)n));
     if ((rc = compute_order(g))) return fail(rc);
+    choose_kernel(g);
     if ((DS_PULL_LIGHT || DS_PULL_HEAVY) && (rc = check_symmetric(g))) return fail(rc);
 #undef CKG
     *out = g;
@@ -1112,6 +1136,10 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
         const char* bh = getenv("DS_BIG_H");
         p.big_light = bl ? (unsigned long long)atoll(bl) : ~0ull;
         p.big_heavy = bh ? (unsigned long long)atoll(bh) : (4ull << 20);
+        const char* le = getenv("DS_LOCAL_E");
+        const char* ln = getenv("DS_LOCAL_N");
+        p.local_edges = le ? (unsigned long long)atoll(le) : 16384ull;
+        p.local_entries = ln ? (unsigned long long)atoll(ln) : 4096ull;
     }
     p.Rpre = g->Rpre;
     p.Rbase = g->Rbase;
@@ -1129,6 +1157,7 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     }
     p.trace = g->trace;
     p.trace_cap = g->trace_cap;
+    if (g->trace) CK(cudaMemsetAsync(g->trace, 0, 2 * sizeof(unsigned long long) * g->trace_cap, g->stream));
     const unsigned grid = (unsigned)(std::is_same<M, ModeFixed>::value ? g->grid_fixed : g->grid_f64);
     CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
     cudaLaunchConfig_t cfg = {};
@@ -1160,7 +1189,10 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     // budget), after which it is relaunched and resumes from Ctl.
     const size_t smem = sizeof(Smem<typename M::D>);
     for (int hop = 0;; ++hop) {
-        CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M>, p));
+        if (g->small)
+            CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M, true>, p));
+        else
+            CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M, false>, p));
         CK(cudaMemcpyAsync(g->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
         CK(cudaStreamSynchronize(g->stream));
         const Ctl& h = *g->h_ctl;
@@ -1181,7 +1213,13 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
         CK(cudaMemsetAsync(g->sbits, 0, sizeof(unsigned) * g->nwords, g->stream));
         CK(cudaStreamSynchronize(g->stream));
     }
-    if (c.abort) return set_err(DS_ETIMEOUT, "solver watchdog expired (DS_TIMEOUT_S=%g)", tmo);
+    if (c.abort) {
+        if (g->trace) {  // keep the partial timeline for post-mortems
+            g->trace_len = g->trace_cap;
+            g->trace_t0 = c.last_bucket;
+        }
+        return set_err(DS_ETIMEOUT, "solver watchdog expired (DS_TIMEOUT_S=%g)", tmo);
+    }
     if (g->trace) {
         g->trace_len = std::min(c.steps, g->trace_cap);
         g->trace_t0 = c.last_bucket;
@@ -1413,6 +1451,7 @@ int ds_internal_adopt(ds_graph** out, int device, void* stream, long long n, lon
     g->w = w;
     int rc = alloc_scratch(g);
     if (!rc) rc = compute_order(g);
+    if (!rc) choose_kernel(g);
     if (!rc && (DS_PULL_LIGHT || DS_PULL_HEAVY)) rc = check_symmetric(g);
     if (rc) {
         free_all(g);

@@ -180,6 +180,12 @@ struct Ctl {
     unsigned long long rs_re, rs_scount, rs_old_scount, rs_pp, rs_bpar;
     long long rs_idx;
     StepSlot xslot;  // results of the standalone push
+    StepSlot lslot[2];  // block-local mode (CTA 0 alone)
+    // results of the block-local steps; light and heavy publish to separate
+    // fields so a slow CTA still reading the light result is never overwritten
+    // by CTA 0 racing ahead into the local heavy step
+    unsigned long long h_phases, h_re, h_pp, h_done, h_status, h_escanned;
+    unsigned long long hh_re, hh_done, hh_status;
 };
 
 enum : int { POS_FRESH = 0, POS_BUCKET = 1, POS_PHASE = 2, POS_AFTER_LIGHT = 3, POS_HEAVY = 4,
@@ -210,6 +216,7 @@ struct KParams {
     int pull_enabled;
     float pull_light, pull_heavy;  // pull when push volume > frac * nnz
     unsigned long long big_light, big_heavy;  // pushes with >= this many edges run standalone
+    unsigned long long local_edges, local_entries;  // SMALL kernel: CTA-0-only steps below these
     long long ceiling;
     unsigned long long timeout_ns;
     const long long* indptr;  // original CSR row offsets (for m_r)
@@ -558,7 +565,7 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
 // ended the previous phase (VALS: the list carries values produced by a pull
 // and this step commits them to t first), looks up degrees in `ptr`, clears
 // the next-frontier dedup bits for their next use, optionally adds to S.
-template <class M, bool APPEND_S, bool VALS>
+template <class M, bool APPEND_S, bool VALS, bool LOCALW = false>
 __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                              const int* list, const typename M::D* vals, unsigned long long count,
                              const long long* ptr, unsigned* clear_bits, int* S,
@@ -569,8 +576,9 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
     unsigned qn = 0;
     const unsigned long long per_chunk = 32ull * kListPer;
     const unsigned long long nchunk = (count + per_chunk - 1) / per_chunk;
-    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
-    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    // LOCALW: only this CTA's warps take part (block-local small-frontier mode)
+    const unsigned long long gw = LOCALW ? wib : (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = LOCALW ? kWarps : (unsigned long long)gridDim.x * kWarps;
     for (unsigned long long c = gw; c < nchunk; c += nw) {
         int vtx[kListPer];
         bool in[kListPer];
@@ -618,7 +626,7 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
 #endif
 // Inlined: a __noinline__ push measured 25% slower (the kernel parameters
 // then live in a local-memory frame).
-template <class M, bool LIGHT>
+template <class M, bool LIGHT, bool LOCALW = false>
 __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                            unsigned long long E, unsigned long long Rc,
                            const typename M::Edge* edges, typename M::D H, int* out_list,
@@ -629,8 +637,8 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     WarpSmem<D>& ws = sm.w[wib];
     unsigned qn = 0;
     const unsigned long long nchunk = (E + kChunk - 1) / kChunk;
-    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
-    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    const unsigned long long gw = LOCALW ? wib : (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = LOCALW ? kWarps : (unsigned long long)gridDim.x * kWarps;
     const unsigned long long pol = evict_first_policy();
     bool overflow = false;
     for (unsigned long long c = gw; c < nchunk; c += nw) {
@@ -907,7 +915,7 @@ __device__ void commit_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSl
 
 // ---------------------------------------------------------------- the solver
 
-template <class M>
+template <class M, bool SMALL>
 __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     sssp_persistent_kernel(const KParams<M> p) {
     using D = typename M::D;
@@ -1058,6 +1066,79 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 handoff(POS_AFTER_LIGHT, 1, E, re >> kPackShift);
                 return;
             }
+            if (SMALL && E <= p.local_edges && (re >> kPackShift) <= p.local_entries) {
+                // ---- block-local mode (high-diameter graphs: tiny frontiers):
+                // CTA 0 runs light phases back to back with block barriers while
+                // the frontier stays small; the other CTAs wait at the next
+                // grid barrier.  Same steps, same snapshot semantics.
+                if (blockIdx.x == 0) {
+                    unsigned long long lre = re, lph = phases, lesc = 0;
+                    int lpp = pp, done = 0, lst = 0, k = 0;
+                    for (;;) {
+                        StepSlot* a = &c->lslot[k];
+                        if (threadIdx.x == 0) {
+                            a->re_packed = a->front_count = a->append_count = 0;
+                            a->flags = 0;
+                        }
+                        __syncthreads();
+                        const unsigned long long lE = lre & kMask33;
+                        lesc += lE;
+                        if (lE)
+                            relax_step<M, true, true>(p, sm, a, lE, lre >> kPackShift, p.Ledges, H,
+                                                      p.F[lpp], p.fbits[lph & 1]);
+                        __syncthreads();
+                        if (ldcg(&a->flags) & 1u) {
+                            lst = kDevOverflow;
+                            break;
+                        }
+                        const unsigned long long lnf = ldcg(&a->append_count);
+                        if (lnf == 0) {
+                            done = 1;
+                            break;
+                        }
+                        k ^= 1;
+                        StepSlot* b = &c->lslot[k];
+                        if (threadIdx.x == 0) {
+                            b->re_packed = b->front_count = b->append_count = 0;
+                            b->flags = 0;
+                        }
+                        __syncthreads();
+                        capture_list<M, true, false, true>(p, sm, b, p.F[lpp], nullptr, lnf, p.Lptr,
+                                                           p.fbits[lph & 1], p.S[bpar],
+                                                           &c->s_count[bpar]);
+                        __syncthreads();
+                        lre = ldcg(&b->re_packed);
+                        lpp ^= 1;
+                        if ((lre & kMask33) > p.local_edges || (lre >> kPackShift) > p.local_entries)
+                            break;  // grown: the next phase runs on the whole grid
+                        ++lph;
+                        if ((long long)lph > p.ceiling) {
+                            lst = 2;
+                            break;
+                        }
+                    }
+                    if (threadIdx.x == 0) {
+                        c->h_phases = lph;
+                        c->h_re = lre;
+                        c->h_pp = (unsigned long long)lpp;
+                        c->h_done = (unsigned long long)done;
+                        c->h_status = (unsigned long long)lst;
+                    }
+                    escanned += lesc;
+                }
+                if (!end_step(9, E)) return;
+                phases = ldcg(&c->h_phases);
+                re = ldcg(&c->h_re);
+                pp = (int)ldcg(&c->h_pp);
+                status = (int)ldcg(&c->h_status);
+                if (status) break;
+                if (ldcg(&c->h_done)) {
+                    pos = POS_HEAVY;
+                } else {
+                    pos = POS_PHASE;
+                    continue;
+                }
+            } else {
             if (DS_PULL_LIGHT && E > pullL) {
                 escanned += (unsigned long long)p.Lpull.nnz;
                 ++npull;
@@ -1095,6 +1176,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 nf = ldcg(&prev()->append_count);
             }
             pos = POS_AFTER_LIGHT;
+            }
         } else if (pos == POS_AFTER_LIGHT && resumed) {
             // results of the standalone light push
             resumed = false;
@@ -1122,11 +1204,47 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         if (pos == POS_HEAVY) {
             // ---- heavy relaxation from S with current t (sssp.py:218-227)
             scount = ldcg(&c->s_count[bpar]);
-            capture_list<M, false, false>(p, sm, &c->slot[st % 3], p.S[bpar], nullptr, scount,
-                                          p.Hptr, nullptr, nullptr, nullptr);
-            if (!end_step(3, scount)) return;
-            re = ldcg(&prev()->re_packed);
-            const unsigned long long E = re & kMask33;
+            bool heavy_done = false;
+            if (SMALL && scount <= p.local_entries) {
+                // block-local heavy step: CTA 0 captures S and, if small, relaxes it
+                if (blockIdx.x == 0) {
+                    StepSlot* a = &c->lslot[0];
+                    if (threadIdx.x == 0) {
+                        a->re_packed = a->front_count = a->append_count = 0;
+                        a->flags = 0;
+                    }
+                    __syncthreads();
+                    capture_list<M, false, false, true>(p, sm, a, p.S[bpar], nullptr, scount, p.Hptr,
+                                                        nullptr, nullptr, nullptr);
+                    __syncthreads();
+                    const unsigned long long lre = ldcg(&a->re_packed);
+                    int done = 0;
+                    if ((lre & kMask33) <= p.local_edges) {
+                        escanned += lre & kMask33;
+                        if (lre & kMask33)
+                            relax_step<M, false, true>(p, sm, a, lre & kMask33, lre >> kPackShift,
+                                                       p.Hedges, H, nullptr, nullptr);
+                        __syncthreads();
+                        done = 1;
+                    }
+                    if (threadIdx.x == 0) {
+                        c->hh_re = lre;
+                        c->hh_done = (unsigned long long)done;
+                        c->hh_status = (ldcg(&a->flags) & 1u) ? (unsigned long long)kDevOverflow : 0ull;
+                    }
+                }
+                if (!end_step(10, scount)) return;
+                re = ldcg(&c->hh_re);
+                status = (int)ldcg(&c->hh_status);
+                if (status) break;
+                heavy_done = ldcg(&c->hh_done) != 0;
+            } else {
+                capture_list<M, false, false>(p, sm, &c->slot[st % 3], p.S[bpar], nullptr, scount,
+                                              p.Hptr, nullptr, nullptr, nullptr);
+                if (!end_step(3, scount)) return;
+                re = ldcg(&prev()->re_packed);
+            }
+            const unsigned long long E = heavy_done ? 0ull : (re & kMask33);
             if (E >= p.big_heavy) {
                 handoff(POS_AFTER_HEAVY, 2, E, re >> kPackShift);
                 return;

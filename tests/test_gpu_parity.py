@@ -322,3 +322,20 @@ def test_giant_push_handoff_is_exact():
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "handoff ok" in r.stdout
+
+
+def test_block_local_kernel_is_exact():
+    """The small-frontier kernel (CTA-0-only phases) forced on for every graph
+    shape, with tiny and large local thresholds."""
+    import os
+    import subprocess
+    import sys
+
+    from paper_1911_06895_b200.build import REPO
+
+    for le in ("64", "100000"):
+        env = dict(os.environ, DS_SMALL="1", DS_LOCAL_E=le, REPO=REPO)
+        r = subprocess.run([sys.executable, "-c", _HANDOFF_SCRIPT], env=env, capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "handoff ok" in r.stdout
