@@ -5,16 +5,19 @@
 Workload (BASELINE.json configs[3], the single-GPU headline): R-MAT scale 24,
 edge factor 16, a,b,c,d = .57,.19,.19,.05, symmetrised + deduplicated,
 fp32-lattice weights, delta = 0.1, seeded random sources with nonzero degree.
-One step = one batch of `--batch` sources solved on the resident graph.
+One step = one batch of `--batch` sources solved on the resident graph through
+ds_sssp_batch, `--concurrency` sources in flight on SM-disjoint persistent
+grids (each source's result is exactly its single-source result).
 
 * value  : GTEPS = sum(m_r) / device time of the K timed steps (graph and its
            light/heavy split already in HBM; CUDA events on the solver's
            stream; max over ranks).  m_r = out-degree sum of reached vertices.
 * e2e    : the same metric through the public API with HOST buffers: every
            step uploads the CSR from pinned host memory, splits it, solves the
-           batch and copies every distance vector back (SparseVector shape).
+           batch and copies every dense float64 distance vector back.
 * roofline: algorithmic bytes per solve B_alg = 8 m_r + 16 n_r + 8 n
-            / mean kernel time vs MEASURED_PEAKS.json hbm_gbs.
+            / mean kernel time vs MEASURED_PEAKS.json hbm_gbs
+           (with concurrent launches: sum of B_alg / device time of the steps).
 * cpu_baseline: the reference algorithm restated in C (oracle/, OpenMP) on
            the box's host cores, one source of the same graph.
 
@@ -54,6 +57,8 @@ def parse():
     ap.add_argument("--delta", type=float, default=0.1)
     ap.add_argument("--batch", type=int, default=8, help="sources per step (per rank)")
     ap.add_argument("--sources", type=int, default=64, help="source pool (BASELINE: 64)")
+    ap.add_argument("--concurrency", type=int, default=1,
+                    help="sources in flight per GPU (ds_sssp_batch contexts; 1 = one at a time)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
@@ -384,10 +389,14 @@ def main():
     info = g.prepare(delta)
 
     # ---- device-resident timing (value)
-    launches_per_solve = 1
+    conc = max(1, args.concurrency)
+
+    def solve_step(step):
+        stats, _ = g.solve_batch(batch(step), delta, concurrency=conc, keep=False)
+        return stats
+
     for w in range(args.warmup):
-        for s in batch(w):
-            g.solve(s, delta)
+        solve_step(w)
     barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
@@ -401,8 +410,7 @@ def main():
     balg_tot = 0
     ev0.record(stream)
     for k in range(args.steps):
-        for s in batch(args.warmup + k):
-            st = g.solve(s, delta)
+        for s, st in zip(batch(args.warmup + k), solve_step(args.warmup + k)):
             per_solve.append(st.as_dict() | {"source": s})
             m_tot += st.edges_reached
             balg_tot += b_alg(st.edges_reached, st.reached, n)
@@ -425,7 +433,12 @@ def main():
     mean_kern = sum(kern_ms) / len(kern_ms)
     balg_mean = balg_tot / len(per_solve)
     peak, peak_kind = measured_peaks()
-    achieved = balg_mean / (mean_kern * 1e-3) / 1e9
+    if conc == 1:
+        achieved = balg_mean / (mean_kern * 1e-3) / 1e9
+    else:
+        # concurrent launches overlap: aggregate algorithmic bytes over the
+        # device time of the steps (which hold only the solver launches)
+        achieved = balg_tot / (t_ms * 1e-3) / 1e9
     traffic, traffic_src = ncu_traffic()
 
     # ---- delta sweep (informational)
@@ -444,37 +457,24 @@ def main():
     # ---- end to end through the public API with host buffers (e2e)
     e2e = None
     if not args.no_e2e:
-        idx_buf = torch.empty(n, dtype=torch.int64).pin_memory()
-        val_buf = torch.empty(n, dtype=torch.float64).pin_memory()
+        dist_buf = torch.empty((args.batch, n), dtype=torch.float64).pin_memory()
         h2d = pin_indptr.numel() * 8 + pin_col.numel() * 4 + pin_val.numel() * 4
-        e2e_launch = 0
+        d2h = dist_buf.numel() * 8
 
         def e2e_step(step):
-            nonlocal e2e_launch
-            d2h = 0
-            m = 0
             hg = DeviceGraph.from_csr(n, pin_indptr, pin_col, pin_val, device=local, stream=sptr)
-            e2e_launch += 3  # indptr check, column check, weight widening
-            for s in batch(step):
-                st = hg.solve(s, delta)  # first call also splits (prepare)
-                idx, vals = hg.result_sparse(out=(idx_buf.numpy(), val_buf.numpy()))
-                d2h += int(st.reached) * 16
-                m += st.edges_reached
-                e2e_launch += 4  # solver + compaction (count, scan, write)
-            e2e_launch += 4  # split: count, 2 scans, scatter
+            # split + concurrent solves + every distance vector back to the host
+            stats, _ = hg.solve_batch(batch(step), delta, concurrency=conc, out=dist_buf.numpy())
             hg.close()
-            return d2h, m
+            return sum(st.edges_reached for st in stats)
 
         e2e_step(0)
         barrier()
         torch.cuda.synchronize()
-        e2e_launch = 0
         t0 = time.perf_counter()
-        d2h_tot, m_e2e = 0, 0
+        m_e2e = 0
         for k in range(args.steps):
-            d, m = e2e_step(args.warmup + k)
-            d2h_tot += d
-            m_e2e += m
+            m_e2e += e2e_step(args.warmup + k)
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
         if pg is not None:
@@ -485,10 +485,10 @@ def main():
             pg.all_reduce(mm)
             m_e2e = float(mm.item())
         e2e = {"value": m_e2e / t_e2e / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h_tot // args.steps,
+               "d2h_bytes_per_step": d2h,
                "ms_per_step": t_e2e / args.steps * 1e3,
-               "includes": "pinned H2D of the CSR, device split, batch solves, D2H of "
-                           "every SparseVector (indices int64 + values f64)"}
+               "includes": "pinned H2D of the CSR, device validation + split, the batch's "
+                           "solves, D2H of every dense float64 distance vector"}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -522,6 +522,7 @@ def main():
                 "n": n, "nnz": nnz, "nnz_light": int(info.nnz_light),
                 "nnz_heavy": int(info.nnz_heavy), "sources_per_step": args.batch,
                 "source_pool": args.sources, "parallelism": f"replicas{ws}",
+                "concurrency": conc,
                 "l2": "inputs larger than L2 (CSR %.1f GB)" % (nnz * 8 / 1e9),
             },
             "roofline": {
@@ -537,10 +538,13 @@ def main():
                 "kernel": "ds::sssp_persistent_kernel<ModeFixed>",
                 "algorithmic_bytes_per_launch": balg_mean,
                 "mean_launch_ms": mean_kern,
+                "achieved_basis": ("bytes per launch / mean launch time" if conc == 1 else
+                                   f"{conc} concurrent launches: sum of algorithmic bytes / "
+                                   "device time of the timed steps"),
             },
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_solve * len(per_solve),
+            "gpu_launches": sum(p["launches"] for p in per_solve),
             "clocks": clk,
             "solver": {
                 "gteps_kernel": m_tot / (sum(kern_ms) * 1e-3) / 1e9,

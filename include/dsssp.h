@@ -13,6 +13,7 @@
  *                         + phase ceiling                      sssp.py:268-274
  *   ds_sssp            <- delta_stepping(matrix, source, delta,
  *                           skip_empty_buckets=...)            sssp.py:239-313
+ *   ds_sssp_batch      <- the callers' per-source loop          cli.py:119-128
  *   ds_result_sparse   <- SsspResult.distances (SparseVector)  sssp.py:82-87,
  *                                                              core.py:46-70
  *   ds_result_dense    <- same, as a dense float64 vector (+inf = absent)
@@ -85,6 +86,7 @@ typedef struct ds_stats {
     int32_t dist_mode;        /* mode that produced the result            */
     int32_t fallbacks;        /* 1 if fixed-point overflowed and f64 reran */
     int64_t pull_steps;       /* relaxations run in pull (vxm) form       */
+    int64_t launches;         /* solver kernel launches (persistent + handed-off pushes) */
 } ds_stats;
 
 /* Upload a CSR adjacency (rows = out-edges).  indptr: n+1 int64; col: nnz
@@ -102,6 +104,17 @@ int ds_graph_prepare(ds_graph* g, double delta, uint32_t flags, ds_prep_info* in
 /* One source, end to end on the device (prepares if needed).  Result stays
  * on the device until fetched with ds_result_*. stats may be NULL. */
 int ds_sssp(ds_graph* g, int64_t source, double delta, uint32_t flags, ds_stats* stats);
+
+/* k sources against one prepared graph (the reference's callers loop over
+ * sources: cli.py:119-128, the 64/16-source benchmarks).  Up to `concurrency`
+ * sources run at once on SM-disjoint persistent grids, each on its own
+ * stream (0 = library default, DS_BATCH_CONC or 2).  stats: k entries or
+ * NULL.  dist_out: k x n float64 (row i = dense distances of sources[i],
+ * +inf = unreachable), host or device, or NULL to keep nothing.  A source
+ * whose fixed-point solve overflows is rerun in binary64 (stats.fallbacks=1).
+ * Leaves no "last result" for ds_result_*. */
+int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, double delta, uint32_t flags,
+                  int32_t concurrency, ds_stats* stats, double* dist_out);
 
 /* Dense float64 distances of the last solve (+inf = unreachable); out holds
  * n doubles, host or device. */

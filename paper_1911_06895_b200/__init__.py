@@ -22,6 +22,7 @@ from .sssp import (  # noqa: F401
     bucket_bounds,
     clear_device_cache,
     delta_stepping,
+    delta_stepping_batch,
     split_edges,
 )
 
@@ -41,6 +42,7 @@ __all__ = [
     "bucket_bounds",
     "clear_device_cache",
     "delta_stepping",
+    "delta_stepping_batch",
     "split_edges",
     "__version__",
 ]

@@ -20,7 +20,8 @@ DS_MODE_FIXED32, DS_MODE_F64 = 0, 1
 
 # Every entry point include/dsssp.h declares (checked by the CPU tests).
 EXPORTS = (
-    "ds_graph_create", "ds_graph_prepare", "ds_sssp", "ds_result_dense", "ds_result_sparse",
+    "ds_graph_create", "ds_graph_prepare", "ds_sssp", "ds_sssp_batch", "ds_result_dense",
+    "ds_result_sparse",
     "ds_export_split", "ds_graph_set_stream", "ds_graph_size", "ds_graph_destroy",
     "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download", "ds_debug_trace",
     "ds_shard_create", "ds_shard_destroy", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",
@@ -55,6 +56,7 @@ class Stats(ctypes.Structure):
         ("dist_mode", ctypes.c_int32),
         ("fallbacks", ctypes.c_int32),
         ("pull_steps", ctypes.c_int64),
+        ("launches", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:
@@ -94,6 +96,8 @@ def lib():
         L.ds_graph_prepare.argtypes = [_vp, ctypes.c_double, ctypes.c_uint32,
                                        ctypes.POINTER(PrepInfo)]
         L.ds_sssp.argtypes = [_vp, _i64, ctypes.c_double, ctypes.c_uint32, ctypes.POINTER(Stats)]
+        L.ds_sssp_batch.argtypes = [_vp, _vp, _i64, ctypes.c_double, ctypes.c_uint32, ctypes.c_int32,
+                                    _vp, _vp]
         L.ds_result_dense.argtypes = [_vp, _vp]
         L.ds_result_sparse.argtypes = [_vp, _vp, _vp]
         L.ds_export_split.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp]

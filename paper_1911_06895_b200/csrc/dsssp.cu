@@ -19,7 +19,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/dsssp.h"
 #include "common.cuh"
@@ -160,6 +163,33 @@ struct PrepStats {
     unsigned long long nL, nH;
 };
 
+// Per-solve scratch and control.  The handle's own buffers form context 0
+// (ds_sssp); ds_sssp_batch adds contexts so that several sources solve
+// concurrently on SM-disjoint persistent grids, each on its own stream.
+struct SolveCtx {
+    cudaStream_t stream = nullptr;
+    void* dist = nullptr;
+    unsigned* fbits = nullptr;
+    unsigned* sbits = nullptr;
+    int *F0 = nullptr, *F1 = nullptr, *S0 = nullptr, *S1 = nullptr;
+    void *Fv0 = nullptr, *Fv1 = nullptr, *req = nullptr;
+    long long *Rpre = nullptr, *Rbase = nullptr;
+    void* Rd = nullptr;
+    unsigned* chunk_start = nullptr;
+    Ctl* ctl = nullptr;
+    Ctl* h_ctl = nullptr;
+    double* out = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ready = nullptr;
+    bool traced = false;  // only context 0 records the DS_TRACE timeline
+    bool owned = false;   // extra contexts own their buffers and stream
+    long long launches = 0;  // kernel launches of the last solve
+    // batch result streaming: a second output buffer and a copy stream so the
+    // D2H of one source overlaps the next source's solve
+    double* out2 = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr};
+};
+
 struct ds_graph {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -233,7 +263,43 @@ struct ds_graph {
     unsigned long long trace_cap = 0;
     unsigned long long trace_len = 0;
     long long trace_t0 = 0;
+    std::vector<SolveCtx*> extra;  // batch contexts 1.. (lazily created)
+    cudaStream_t batch_stream = nullptr;  // context 0's stream inside a batch
+    cudaEvent_t batch_ev = nullptr;
+    double* out2 = nullptr;  // context 0's second batch output buffer
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr};
 };
+
+static SolveCtx main_ctx(ds_graph* g) {
+    SolveCtx x;
+    x.stream = g->stream;
+    x.dist = g->dist;
+    x.fbits = g->fbits;
+    x.sbits = g->sbits;
+    x.F0 = g->F0;
+    x.F1 = g->F1;
+    x.S0 = g->S0;
+    x.S1 = g->S1;
+    x.Fv0 = g->Fv0;
+    x.Fv1 = g->Fv1;
+    x.req = g->req;
+    x.Rpre = g->Rpre;
+    x.Rbase = g->Rbase;
+    x.Rd = g->Rd;
+    x.chunk_start = g->chunk_start;
+    x.ctl = g->ctl;
+    x.h_ctl = g->h_ctl;
+    x.out = g->out;
+    x.ev0 = g->ev0;
+    x.ev1 = g->ev1;
+    x.traced = true;
+    x.out2 = g->out2;
+    x.copy_stream = g->copy_stream;
+    x.copied[0] = g->copied[0];
+    x.copied[1] = g->copied[1];
+    return x;
+}
 
 static void free_all(ds_graph* g) {
     void* ptrs[] = {g->indptr, g->col,  g->w,     g->Lptr,  g->Hptr,       g->Ledges, g->Hedges,
@@ -244,6 +310,28 @@ static void free_all(ds_graph* g) {
                     g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (SolveCtx* x : g->extra) {
+        void* q[] = {x->dist, x->fbits, x->sbits, x->F0, x->F1, x->S0, x->S1, x->Fv0, x->Fv1,
+                     x->req, x->Rpre, x->Rbase, x->Rd, x->chunk_start, x->ctl, x->out, x->out2};
+        for (void* p : q)
+            if (p) cudaFree(p);
+        for (cudaEvent_t e : x->copied)
+            if (e) cudaEventDestroy(e);
+        if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
+        delete x->h_ctl;
+        if (x->ev0) cudaEventDestroy(x->ev0);
+        if (x->ev1) cudaEventDestroy(x->ev1);
+        if (x->ready) cudaEventDestroy(x->ready);
+        if (x->stream) cudaStreamDestroy(x->stream);
+        delete x;
+    }
+    g->extra.clear();
+    if (g->batch_ev) cudaEventDestroy(g->batch_ev);
+    if (g->out2) cudaFree(g->out2);
+    for (cudaEvent_t e : g->copied)
+        if (e) cudaEventDestroy(e);
+    if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+    if (g->batch_stream) cudaStreamDestroy(g->batch_stream);
     delete g->h_ctl;  // small pageable mirrors (cudaFreeHost costs ms per call)
     delete g->h_pstat;
     if (g->ev0) cudaEventDestroy(g->ev0);
@@ -263,6 +351,7 @@ static bool is_device_ptr(const void* p) {
 static unsigned grid_blocks_for(int nsm, int occ) {
     int per = std::max(1, std::min(occ, 8));
     if (const char* s = getenv("DS_BLOCKS_PER_SM")) per = std::max(1, std::min(per, atoi(s)));
+    if (const char* s = getenv("DS_GRID_SMS")) nsm = std::max(1, std::min(nsm, atoi(s)));  // probe knob
     return (unsigned)(nsm * per);
 }
 
@@ -1094,8 +1183,12 @@ extern "C" int ds_graph_prepare(ds_graph* g, double delta, uint32_t flags, ds_pr
     return DS_OK;
 }
 
+static unsigned full_grid(const ds_graph* g) {
+    return (unsigned)(g->mode == DS_MODE_FIXED32 ? g->grid_fixed : g->grid_f64);
+}
+
 template <class M>
-static int launch_solve(ds_graph* g, long long source, int* dev_status) {
+static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned grid, int* dev_status) {
     KParams<M> p{};
     p.n = g->n;
     p.source = source;
@@ -1110,17 +1203,17 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     p.Ledges = (const typename M::Edge*)g->Ledges;
     p.Hptr = g->Hptr;
     p.Hedges = (const typename M::Edge*)g->Hedges;
-    p.dist = (typename M::D*)g->dist;
-    p.fbits[0] = g->fbits;
-    p.fbits[1] = g->fbits + g->nwords;
-    p.sbits = g->sbits;
-    p.F[0] = g->F0;
-    p.F[1] = g->F1;
-    p.Fv[0] = (typename M::D*)g->Fv0;
-    p.Fv[1] = (typename M::D*)g->Fv1;
-    p.S[0] = g->S0;
-    p.S[1] = g->S1;
-    p.req = (typename M::D*)g->req;
+    p.dist = (typename M::D*)x.dist;
+    p.fbits[0] = x.fbits;
+    p.fbits[1] = x.fbits + g->nwords;
+    p.sbits = x.sbits;
+    p.F[0] = x.F0;
+    p.F[1] = x.F1;
+    p.Fv[0] = (typename M::D*)x.Fv0;
+    p.Fv[1] = (typename M::D*)x.Fv1;
+    p.S[0] = x.S0;
+    p.S[1] = x.S1;
+    p.req = (typename M::D*)x.req;
     p.Lpull = {g->planL.rowid, g->planL.cptr, g->planL.chunk_row, g->planL.span, g->planL.n_nz,
                g->planL.nspan, g->planL.nnz};
     p.Hpull = {g->planH.rowid, g->planH.cptr, g->planH.chunk_row, g->planH.span, g->planH.n_nz,
@@ -1136,35 +1229,40 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
         const char* bh = getenv("DS_BIG_H");
         p.big_light = bl ? (unsigned long long)atoll(bl) : ~0ull;
         p.big_heavy = bh ? (unsigned long long)atoll(bh) : (4ull << 20);
+        if (grid < full_grid(g)) {
+            // concurrent batch contexts: a full-device standalone push would
+            // stall the other contexts' grids (measured slower), so no handoff
+            p.big_light = p.big_heavy = ~0ull;
+        }
         const char* le = getenv("DS_LOCAL_E");
         const char* ln = getenv("DS_LOCAL_N");
         p.local_edges = le ? (unsigned long long)atoll(le) : 16384ull;
         p.local_entries = ln ? (unsigned long long)atoll(ln) : 4096ull;
     }
-    p.Rpre = g->Rpre;
-    p.Rbase = g->Rbase;
-    p.Rd = (typename M::D*)g->Rd;
-    p.chunk_start = g->chunk_start;
+    p.Rpre = x.Rpre;
+    p.Rbase = x.Rbase;
+    p.Rd = (typename M::D*)x.Rd;
+    p.chunk_start = x.chunk_start;
     p.perm = g->perm;
     p.n_active = g->n_active;
-    p.ctl = g->ctl;
-    p.out = g->out;
-    if (const char* tr = getenv("DS_TRACE")) {
+    p.ctl = x.ctl;
+    p.out = x.out;
+    if (const char* tr = getenv("DS_TRACE"); tr && x.traced) {
         if (atoi(tr) && !g->trace) {
             g->trace_cap = 1 << 20;
             CK(cudaMalloc(&g->trace, 2 * sizeof(unsigned long long) * g->trace_cap));
         }
     }
-    p.trace = g->trace;
+    unsigned long long* trace = x.traced ? g->trace : nullptr;
+    p.trace = trace;
     p.trace_cap = g->trace_cap;
-    if (g->trace) CK(cudaMemsetAsync(g->trace, 0, 2 * sizeof(unsigned long long) * g->trace_cap, g->stream));
-    const unsigned grid = (unsigned)(std::is_same<M, ModeFixed>::value ? g->grid_fixed : g->grid_f64);
-    CK(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), g->stream));
+    if (trace) CK(cudaMemsetAsync(trace, 0, 2 * sizeof(unsigned long long) * g->trace_cap, x.stream));
+    CK(cudaMemsetAsync(x.ctl, 0, sizeof(Ctl), x.stream));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = sizeof(Smem<typename M::D>);
-    cfg.stream = g->stream;
+    cfg.stream = x.stream;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeCooperative;
     at[0].val.cooperative = 1;
@@ -1173,7 +1271,7 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     const size_t dbytes = sizeof(typename M::D) * (size_t)g->n;
     if (g->persist_bytes > 0) {
         at[1].id = cudaLaunchAttributeAccessPolicyWindow;
-        at[1].val.accessPolicyWindow.base_ptr = g->dist;
+        at[1].val.accessPolicyWindow.base_ptr = x.dist;
         at[1].val.accessPolicyWindow.num_bytes = std::min(dbytes, g->max_window);
         at[1].val.accessPolicyWindow.hitRatio =
             (float)std::min(1.0, (double)g->persist_bytes / (double)at[1].val.accessPolicyWindow.num_bytes);
@@ -1183,49 +1281,81 @@ static int launch_solve(ds_graph* g, long long source, int* dev_status) {
     }
     cfg.attrs = at;
     cfg.numAttrs = nattr;
-    CK(cudaEventRecord(g->ev0, g->stream));
+    CK(cudaEventRecord(x.ev0, x.stream));
     // The persistent kernel runs the whole solve on the device; it only stops
     // to hand a giant push to k_big_relax (its own launch and register
     // budget), after which it is relaunched and resumes from Ctl.
     const size_t smem = sizeof(Smem<typename M::D>);
+    x.launches = 0;
     for (int hop = 0;; ++hop) {
+        ++x.launches;
         if (g->small)
             CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M, true>, p));
         else
             CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M, false>, p));
-        CK(cudaMemcpyAsync(g->h_ctl, g->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, g->stream));
-        CK(cudaStreamSynchronize(g->stream));
-        const Ctl& h = *g->h_ctl;
+        CK(cudaMemcpyAsync(x.h_ctl, x.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, x.stream));
+        CK(cudaStreamSynchronize(x.stream));
+        const Ctl& h = *x.h_ctl;
         if (h.abort || h.status != 0 || h.rs_req == 0) break;
         const unsigned rgrid = (unsigned)(g->nsm * (h.rs_req == 1 ? g->occ_big_l : g->occ_big_h));
+        ++x.launches;
         if (h.rs_req == 1)
-            k_big_relax<M, true><<<rgrid, kThreads, smem, g->stream>>>(p);
+            k_big_relax<M, true><<<rgrid, kThreads, smem, x.stream>>>(p);
         else
-            k_big_relax<M, false><<<rgrid, kThreads, smem, g->stream>>>(p);
+            k_big_relax<M, false><<<rgrid, kThreads, smem, x.stream>>>(p);
         CK(cudaGetLastError());
     }
-    CK(cudaEventRecord(g->ev1, g->stream));
-    CK(cudaStreamSynchronize(g->stream));
-    const Ctl& c = *g->h_ctl;
+    CK(cudaEventRecord(x.ev1, x.stream));
+    CK(cudaStreamSynchronize(x.stream));
+    const Ctl& c = *x.h_ctl;
     // an interrupted solve may leave dedup bits set: clear them for the next one
     if (c.abort || c.status != 0) {
-        CK(cudaMemsetAsync(g->fbits, 0, 2 * sizeof(unsigned) * g->nwords, g->stream));
-        CK(cudaMemsetAsync(g->sbits, 0, sizeof(unsigned) * g->nwords, g->stream));
-        CK(cudaStreamSynchronize(g->stream));
+        CK(cudaMemsetAsync(x.fbits, 0, 2 * sizeof(unsigned) * g->nwords, x.stream));
+        CK(cudaMemsetAsync(x.sbits, 0, sizeof(unsigned) * g->nwords, x.stream));
+        CK(cudaStreamSynchronize(x.stream));
     }
     if (c.abort) {
-        if (g->trace) {  // keep the partial timeline for post-mortems
+        if (trace) {  // keep the partial timeline for post-mortems
             g->trace_len = g->trace_cap;
             g->trace_t0 = c.last_bucket;
         }
         return set_err(DS_ETIMEOUT, "solver watchdog expired (DS_TIMEOUT_S=%g)", tmo);
     }
-    if (g->trace) {
+    if (trace) {
         g->trace_len = std::min(c.steps, g->trace_cap);
         g->trace_t0 = c.last_bucket;
     }
     *dev_status = c.status;
     return DS_OK;
+}
+
+// SsspResult counters + device stats of a finished solve (sssp.py:82-87)
+static void fill_stats(ds_graph* g, const SolveCtx& x, double delta, uint32_t flags, int fallbacks,
+                       ds_stats* stats) {
+    const Ctl& c = *x.h_ctl;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, x.ev0, x.ev1);
+    double maxd;
+    if (g->mode == DS_MODE_FIXED32)
+        maxd = ldexp((double)(unsigned)c.max_d, -g->frac);
+    else
+        memcpy(&maxd, &c.max_d, 8);
+    stats->inner_phases = (int64_t)c.phases;
+    stats->buckets_visited = (int64_t)c.visited;
+    // non-skip outer loop stops at the first i with max(t) < i*delta
+    // (sssp.py:280), i.e. bucket_index_of(max t) + 1
+    const long long nonskip = bucket_index_of(maxd, delta) + 1;
+    stats->outer_iterations = (flags & DS_FLAG_SKIP_EMPTY) ? (int64_t)c.visited : nonskip;
+    stats->reached = (int64_t)c.reached;
+    stats->edges_reached = (int64_t)c.edges_reached;
+    stats->edges_scanned = (int64_t)c.edges_scanned;
+    stats->grid_barriers = (int64_t)c.barriers;
+    stats->max_distance = maxd;
+    stats->kernel_ms = ms;
+    stats->dist_mode = g->mode;
+    stats->fallbacks = fallbacks;
+    stats->pull_steps = (int64_t)c.pulls;
+    stats->launches = x.launches;
 }
 
 extern "C" int ds_sssp(ds_graph* g, int64_t source, double delta, uint32_t flags, ds_stats* stats) {
@@ -1237,12 +1367,14 @@ extern "C" int ds_sssp(ds_graph* g, int64_t source, double delta, uint32_t flags
         return set_err(DS_EINVAL, "delta must be a positive finite number, got %g", delta);
     DeviceGuard guard(g->device);
     int fallbacks = 0;
+    SolveCtx x;
     for (;;) {
         int rc = prepare(g, delta, flags);
         if (rc) return rc;
+        x = main_ctx(g);
         int st = 0;
-        rc = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, source, &st)
-                                        : launch_solve<ModeF64>(g, source, &st);
+        rc = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, x, source, full_grid(g), &st)
+                                        : launch_solve<ModeF64>(g, x, source, full_grid(g), &st);
         if (rc) return rc;
         if (st == kDevOverflow) {
             // a fixed-point distance would exceed 32 bits: redo in binary64
@@ -1258,33 +1390,194 @@ extern "C" int ds_sssp(ds_graph* g, int64_t source, double delta, uint32_t flags
         if (st != 0) return set_err(DS_ECUDA, "device solver status %d", st);
         break;
     }
-    const Ctl& c = *g->h_ctl;
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-    double maxd;
-    if (g->mode == DS_MODE_FIXED32)
-        maxd = ldexp((double)(unsigned)c.max_d, -g->frac);
-    else
-        memcpy(&maxd, &c.max_d, 8);
     g->have_result = true;
-    g->reached = (long long)c.reached;
-    if (stats) {
-        stats->inner_phases = (int64_t)c.phases;
-        stats->buckets_visited = (int64_t)c.visited;
-        // non-skip outer loop stops at the first i with max(t) < i*delta
-        // (sssp.py:280), i.e. bucket_index_of(max t) + 1
-        const long long nonskip = bucket_index_of(maxd, delta) + 1;
-        stats->outer_iterations = (flags & DS_FLAG_SKIP_EMPTY) ? (int64_t)c.visited : nonskip;
-        stats->reached = (int64_t)c.reached;
-        stats->edges_reached = (int64_t)c.edges_reached;
-        stats->edges_scanned = (int64_t)c.edges_scanned;
-        stats->grid_barriers = (int64_t)c.barriers;
-        stats->max_distance = maxd;
-        stats->kernel_ms = ms;
-        stats->dist_mode = g->mode;
-        stats->fallbacks = fallbacks;
-        stats->pull_steps = (int64_t)c.pulls;
+    g->reached = (long long)x.h_ctl->reached;
+    if (stats) fill_stats(g, x, delta, flags, fallbacks, stats);
+    return DS_OK;
+}
+
+// ---------------------------------------------------------------- batched sources
+
+static int make_ctx(ds_graph* g, SolveCtx** out) {
+    const long long n = g->n;
+    SolveCtx* x = new SolveCtx();
+    x->owned = true;
+    *out = x;
+    g->extra.push_back(x);  // freed with the handle, even on partial failure
+    CK(cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking));
+    CK(cudaMalloc(&x->dist, sizeof(unsigned long long) * n));
+    CK(cudaMalloc(&x->fbits, 2 * sizeof(unsigned) * g->nwords));
+    CK(cudaMalloc(&x->sbits, sizeof(unsigned) * g->nwords));
+    CK(cudaMalloc(&x->F0, sizeof(int) * n));
+    CK(cudaMalloc(&x->F1, sizeof(int) * n));
+    CK(cudaMalloc(&x->S0, sizeof(int) * n));
+    CK(cudaMalloc(&x->S1, sizeof(int) * n));
+    if (DS_PULL_LIGHT || DS_PULL_HEAVY) {
+        CK(cudaMalloc(&x->Fv0, sizeof(unsigned long long) * n));
+        CK(cudaMalloc(&x->Fv1, sizeof(unsigned long long) * n));
+        CK(cudaMalloc(&x->req, sizeof(unsigned long long) * n));
     }
+    CK(cudaMalloc(&x->Rpre, sizeof(long long) * n));
+    CK(cudaMalloc(&x->Rbase, sizeof(long long) * n));
+    CK(cudaMalloc(&x->Rd, sizeof(unsigned long long) * n));
+    CK(cudaMalloc(&x->chunk_start, sizeof(unsigned) * (g->nnz / kChunk + 4)));
+    CK(cudaMalloc(&x->ctl, sizeof(Ctl)));
+    x->h_ctl = new Ctl();
+    CK(cudaMalloc(&x->out, sizeof(double) * n));
+    CK(cudaMemsetAsync(x->fbits, 0, 2 * sizeof(unsigned) * g->nwords, x->stream));
+    CK(cudaMemsetAsync(x->sbits, 0, sizeof(unsigned) * g->nwords, x->stream));
+    CK(cudaEventCreate(&x->ev0));
+    CK(cudaEventCreate(&x->ev1));
+    CK(cudaEventCreateWithFlags(&x->ready, cudaEventDisableTiming));
+    CK(cudaStreamSynchronize(x->stream));
+    return DS_OK;
+}
+
+extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, double delta,
+                             uint32_t flags, int32_t concurrency, ds_stats* stats, double* dist_out) {
+    if (!g) return set_err(DS_EINVAL, "null graph handle");
+    if (k < 0 || (k > 0 && !sources)) return set_err(DS_EINVAL, "invalid source list");
+    for (int64_t i = 0; i < k; ++i)
+        if (!(sources[i] >= 0 && sources[i] < g->n))
+            return set_err(DS_EINVAL, "source %lld out of range for %lld vertices",
+                           (long long)sources[i], (long long)g->n);
+    if (!(delta > 0) || !std::isfinite(delta))
+        return set_err(DS_EINVAL, "delta must be a positive finite number, got %g", delta);
+    if (k == 0) return DS_OK;
+    DeviceGuard guard(g->device);
+    int rc = prepare(g, delta, flags);
+    if (rc) return rc;
+    // concurrency: solver contexts on SM-disjoint grids (0 = library default)
+    int T = concurrency;
+    if (T <= 0) {
+        T = 2;
+        if (const char* e = getenv("DS_BATCH_CONC")) T = std::max(1, atoi(e));
+    }
+    T = (int)std::min<long long>({(long long)T, (long long)k, 8LL, (long long)g->nsm});
+    if (DS_PULL_LIGHT || DS_PULL_HEAVY) T = 1;  // pull state is per handle
+    while ((int)g->extra.size() < T - 1) {
+        SolveCtx* x = nullptr;
+        if ((rc = make_ctx(g, &x))) return rc;
+    }
+    if (dist_out) {  // result streaming resources (context 0 on the handle, others on their ctx)
+        auto streaming = [&](double** out2, cudaStream_t* cs, cudaEvent_t* ev) -> int {
+            if (!*out2) CK(cudaMalloc(out2, sizeof(double) * g->n));
+            if (!*cs) CK(cudaStreamCreateWithFlags(cs, cudaStreamNonBlocking));
+            for (int b = 0; b < 2; ++b)
+                if (!ev[b]) CK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+            return DS_OK;
+        };
+        if ((rc = streaming(&g->out2, &g->copy_stream, g->copied))) return rc;
+        for (int t = 1; t < T; ++t) {
+            SolveCtx* x = g->extra[t - 1];
+            if ((rc = streaming(&x->out2, &x->copy_stream, x->copied))) return rc;
+        }
+    }
+    std::vector<SolveCtx> ctx;
+    ctx.push_back(main_ctx(g));
+    for (int t = 1; t < T; ++t) ctx.push_back(*g->extra[t - 1]);
+    if (T > 1) {
+        // every context on its own non-blocking stream (the handle's stream
+        // may be the legacy default stream, which would serialise them),
+        // ordered after the work already queued on the handle's stream
+        if (!g->batch_stream) CK(cudaStreamCreateWithFlags(&g->batch_stream, cudaStreamNonBlocking));
+        if (!g->batch_ev) CK(cudaEventCreateWithFlags(&g->batch_ev, cudaEventDisableTiming));
+        ctx[0].stream = g->batch_stream;
+        CK(cudaEventRecord(g->batch_ev, g->stream));
+        for (int t = 0; t < T; ++t) CK(cudaStreamWaitEvent(ctx[t].stream, g->batch_ev, 0));
+    }
+    const unsigned grid = T == 1 ? full_grid(g) : std::max(1u, full_grid(g) / (unsigned)T);
+    const long long n = g->n;
+    std::atomic<long long> next(0);
+    std::vector<int> err(T, DS_OK);
+    std::vector<std::string> msg(T);
+    std::vector<std::vector<long long>> redo(T);
+    auto worker = [&](int t) {
+        cudaSetDevice(g->device);
+        SolveCtx& x = ctx[t];
+        double* const outs[2] = {x.out, x.out2};
+        for (long long j = 0;; ++j) {
+            const long long i = next.fetch_add(1);
+            if (i >= k) break;
+            const int b = (int)(j & 1);
+            if (dist_out) {
+                // alternate output buffers; reuse one only after its D2H finished
+                x.out = outs[b];
+                if (j >= 2 && cudaStreamWaitEvent(x.stream, x.copied[b], 0) != cudaSuccess) {
+                    err[t] = set_err(DS_ECUDA, "CUDA error ordering a batch output buffer");
+                    msg[t] = g_err;
+                    next.store(k);
+                    break;
+                }
+            }
+            int st = 0;
+            int r = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, x, sources[i], grid, &st)
+                                               : launch_solve<ModeF64>(g, x, sources[i], grid, &st);
+            if (r == DS_OK && st == kDevOverflow) {
+                redo[t].push_back(i);  // rerun in binary64 after the batch
+                continue;
+            }
+            if (r == DS_OK && st == DS_ENOCONVERGE)
+                r = set_err(DS_ENOCONVERGE,
+                            "light phase count exceeded ceiling %lld; relaxation is not converging",
+                            g->ceiling);
+            else if (r == DS_OK && st != 0)
+                r = set_err(DS_ECUDA, "device solver status %d", st);
+            if (r == DS_OK && stats) fill_stats(g, x, delta, flags, 0, stats + i);
+            if (r == DS_OK && dist_out) {
+                // launch_solve returned after its stream drained: the copy
+                // needs no event and overlaps the next source's solve
+                cudaError_t e = cudaMemcpyAsync(dist_out + i * n, x.out, sizeof(double) * n,
+                                                cudaMemcpyDefault, x.copy_stream);
+                if (e == cudaSuccess) e = cudaEventRecord(x.copied[b], x.copy_stream);
+                if (e != cudaSuccess)
+                    r = set_err(DS_ECUDA, "CUDA error %s copying batch result", cudaGetErrorName(e));
+            }
+            if (r != DS_OK) {
+                err[t] = r;
+                msg[t] = g_err;
+                next.store(k);  // stop the other workers after their current source
+                break;
+            }
+        }
+        if (dist_out && cudaStreamSynchronize(x.copy_stream) != cudaSuccess && err[t] == DS_OK) {
+            err[t] = DS_ECUDA;
+            msg[t] = "CUDA error finishing a batch result copy";
+        }
+        if (cudaStreamSynchronize(x.stream) != cudaSuccess && err[t] == DS_OK) {
+            err[t] = DS_ECUDA;
+            msg[t] = "CUDA error synchronising a batch context";
+        }
+    };
+    if (T == 1) {
+        worker(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t) th.emplace_back(worker, t);
+        for (auto& h : th) h.join();
+    }
+    for (int t = 0; t < T; ++t)
+        if (err[t] != DS_OK) return set_err(err[t], "%s", msg[t].c_str());
+    // the handle's stream continues after every context's work
+    for (int t = 0; t < T && T > 1; ++t) {
+        cudaEvent_t e = t == 0 ? g->batch_ev : ctx[t].ready;
+        CK(cudaEventRecord(e, ctx[t].stream));
+        CK(cudaStreamWaitEvent(g->stream, e, 0));
+    }
+    g->have_result = false;  // batch results are delivered through dist_out
+    for (int t = 0; t < T; ++t)
+        for (long long i : redo[t]) {
+            ds_stats one{};
+            if ((rc = ds_sssp(g, sources[i], delta, flags, &one))) return rc;
+            one.fallbacks = 1;
+            if (stats) stats[i] = one;
+            if (dist_out) {
+                CK(cudaMemcpyAsync(dist_out + i * n, g->out, sizeof(double) * n, cudaMemcpyDefault,
+                                   g->stream));
+                CK(cudaStreamSynchronize(g->stream));
+            }
+            g->have_result = false;
+        }
     return DS_OK;
 }
 

@@ -316,6 +316,21 @@ __device__ __forceinline__ unsigned long long evict_first_policy() {
     return pol;
 }
 
+#ifndef DS_LIGHT_POL
+#define DS_LIGHT_POL 0  // L2 policy of light-edge loads: 0 evict_first, 1 evict_normal, 2 evict_last
+#endif
+__device__ __forceinline__ unsigned long long light_policy() {
+    unsigned long long pol;
+#if DS_LIGHT_POL == 2
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#elif DS_LIGHT_POL == 1
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    return pol;
+}
+
 // set bit v; true iff it was clear (first claim this phase / bucket)
 __device__ __forceinline__ bool claim_bit(unsigned* bits, unsigned v) {
     const unsigned m = 1u << (v & 31);
@@ -639,7 +654,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     const unsigned long long nchunk = (E + kChunk - 1) / kChunk;
     const unsigned long long gw = LOCALW ? wib : (unsigned long long)blockIdx.x * kWarps + wib;
     const unsigned long long nw = LOCALW ? kWarps : (unsigned long long)gridDim.x * kWarps;
-    const unsigned long long pol = evict_first_policy();
+    const unsigned long long pol = LIGHT ? light_policy() : evict_first_policy();
     bool overflow = false;
     for (unsigned long long c = gw; c < nchunk; c += nw) {
         const unsigned long long r0 = ldcg(p.chunk_start + c);

@@ -35,6 +35,7 @@ __all__ = [
     "DeviceGraph",
     "bucket_bounds",
     "delta_stepping",
+    "delta_stepping_batch",
     "split_edges",
     "clear_device_cache",
 ]
@@ -189,6 +190,29 @@ class DeviceGraph:
         self.last_stats = st
         return st
 
+    def solve_batch(self, sources, delta: float, skip_empty_buckets: bool = False,
+                    force_f64: bool = False, concurrency: int = 0, out=None,
+                    keep: bool = True):
+        """k sources through ds_sssp_batch.  Returns (stats list, dist) where
+        dist is a k x n float64 array (`out` if given: host ndarray or a
+        device pointer int) or None when keep=False."""
+        src = np.ascontiguousarray(np.asarray(sources, dtype=np.int64).reshape(-1))
+        k = int(src.size)
+        stats = (_lib.Stats * max(k, 1))()
+        flags = (_lib.DS_FLAG_SKIP_EMPTY if skip_empty_buckets else 0) | (
+            _lib.DS_FLAG_FORCE_F64 if force_f64 else 0)
+        if not keep:
+            dptr, dist = None, None
+        elif isinstance(out, int):
+            dptr, dist = out, None
+        else:
+            dist = out if out is not None else np.empty((k, self.n), dtype=np.float64)
+            dptr = _ptr(dist)
+        _lib.check(_lib.lib().ds_sssp_batch(self._handle(), _ptr(src), k, float(delta), flags,
+                                            int(concurrency), stats, dptr))
+        self.last_stats = None
+        return [stats[i] for i in range(k)], dist
+
     def result_dense(self, out=None) -> np.ndarray:
         if out is None:
             out = np.empty(self.n, dtype=np.float64)
@@ -309,6 +333,49 @@ def delta_stepping(
         elapsed=elapsed,
         device_stats=st.as_dict(),
     )
+
+
+def delta_stepping_batch(
+    matrix,
+    sources,
+    delta: float,
+    *,
+    backend: BackendChoice | None = None,
+    skip_empty_buckets: bool = False,
+    concurrency: int = 0,
+) -> list[SsspResult]:
+    """`delta_stepping` for several sources of one matrix -- the loop the
+    reference's callers run (cli.py:119-128, the 64/16-source benchmarks) --
+    with up to `concurrency` sources in flight on SM-disjoint persistent
+    grids.  Each result equals `delta_stepping(matrix, s, delta, ...)`
+    exactly; `elapsed` is the batch's wall time split evenly."""
+    if backend is None:
+        backend = BackendChoice()
+    srcs = [int(s) for s in sources]
+    for s in srcs:
+        if not 0 <= s < matrix.n:
+            raise ValueError(f"source {s} out of range for {matrix.n} vertices")
+    if not (delta > 0) or not math.isfinite(delta):
+        raise ValueError(f"delta must be a positive finite number, got {delta}")
+    if not srcs:
+        return []
+    start = time.perf_counter()
+    g = _device_graph(matrix)
+    stats, dist = g.solve_batch(srcs, float(delta), skip_empty_buckets=skip_empty_buckets,
+                                concurrency=concurrency)
+    elapsed = (time.perf_counter() - start) / len(srcs)
+    out = []
+    for i, st in enumerate(stats):
+        row = dist[i]
+        idx = np.flatnonzero(np.isfinite(row)).astype(np.int64)
+        out.append(SsspResult(
+            distances=SparseVector(matrix.n, idx, row[idx]),
+            outer_iterations=int(st.outer_iterations),
+            inner_phases=int(st.inner_phases),
+            elapsed=elapsed,
+            device_stats=st.as_dict(),
+        ))
+    return out
 
 
 def split_edges(matrix, delta: float, workers: int = 1, chunks_per_worker: int = 1):

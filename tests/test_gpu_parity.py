@@ -20,6 +20,7 @@ from paper_1911_06895_b200 import (
     SparseMatrix,
     clear_device_cache,
     delta_stepping,
+    delta_stepping_batch,
     graphs,
     matrix_build,
     split_edges,
@@ -339,3 +340,56 @@ def test_block_local_kernel_is_exact():
                            text=True, timeout=900)
         assert r.returncode == 0, r.stdout + r.stderr
         assert "handoff ok" in r.stdout
+
+
+def test_batch_matches_single_solves():
+    """ds_sssp_batch (concurrent contexts on SM-disjoint grids) gives every
+    source exactly the single-source result and counters."""
+    cases = [(graphs.rmat(16, seed=1, weight_seed=2), 0.1, 7),
+             (graphs.grid2d(64, seed=3), 25.0, 3),
+             (graphs.erdos_renyi(1024, seed=0), 3.0, 5)]
+    for a, d, k in cases:
+        g = DeviceGraph.from_matrix(a)
+        srcs = list(graphs.pick_sources(a.indptr, k, seed=3))
+        for skip, f64 in ((False, False), (True, True)):
+            want = []
+            for s in srcs:
+                st = g.solve(s, d, skip_empty_buckets=skip, force_f64=f64)
+                want.append((st.inner_phases, st.outer_iterations, st.reached, st.edges_reached,
+                             g.result_dense()))
+            for conc in (1, 2, 3):
+                stats, dist = g.solve_batch(srcs, d, skip_empty_buckets=skip, force_f64=f64,
+                                            concurrency=conc)
+                assert dist.shape == (k, a.n)
+                for i, st in enumerate(stats):
+                    assert (st.inner_phases, st.outer_iterations, st.reached,
+                            st.edges_reached) == want[i][:4], (conc, i)
+                    assert bits_equal(dist[i], want[i][4]), (conc, i)
+                    assert st.dist_mode == (1 if f64 else 0)
+        # the handle keeps working for single solves after a batch
+        st = g.solve(srcs[0], d)
+        assert bits_equal(g.result_dense(), want[0][4])
+        g.close()
+
+
+def test_batch_public_api_vs_oracle_and_overflow():
+    a = graphs.erdos_renyi(1024, seed=0)
+    srcs = list(range(0, 1024, 101))
+    res = delta_stepping_batch(a, srcs, 3.0, concurrency=3)
+    for s, r in zip(srcs, res):
+        want, outer, phases = oracle.delta_stepping(a.n, a.indptr, a.col, a.val, s, 3.0)
+        assert bits_equal(r.distances.to_dense(), want), s
+        assert (r.outer_iterations, r.inner_phases) == (outer, phases)
+        assert r.distances == delta_stepping(a, s, 3.0).distances
+    # sources whose fixed-point distances overflow are rerun in binary64
+    w = float(2**31)
+    b = matrix_build(4, [(0, 1, w), (1, 2, w), (2, 3, w)])
+    res = delta_stepping_batch(b, [0, 1, 2, 3], 1e9, concurrency=2)
+    for s, r in zip([0, 1, 2, 3], res):
+        want, outer, phases = oracle.delta_stepping(4, b.indptr, b.col, b.val, s, 1e9)
+        assert bits_equal(r.distances.to_dense(), want), s
+        assert (r.outer_iterations, r.inner_phases) == (outer, phases)
+    assert res[0].device_stats["fallbacks"] == 1
+    assert delta_stepping_batch(a, [], 3.0) == []
+    with pytest.raises(ValueError, match="out of range"):
+        delta_stepping_batch(a, [0, 5000], 3.0)
