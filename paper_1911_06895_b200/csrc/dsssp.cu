@@ -405,49 +405,71 @@ __device__ __forceinline__ int frac_bits(double w) {
 __device__ __forceinline__ bool light_w(double w, double delta) { return w > 0.0 && w <= delta; }
 __device__ __forceinline__ bool heavy_w(double w, double delta) { return w > delta && w < CUDART_INF; }
 
-// warp per row: light/heavy counts, min light weight, fixed-point eligibility
-// Input rows are read in input order (sequential, coalesced); input row v
-// becomes output row perm[v] (identity when perm == nullptr) and columns are
-// renamed through perm -- the solver's degree-sorted relabeling.
-__global__ void k_split_count(long long n, const long long* indptr, const double* w, double delta,
-                              const int* perm, long long* Lcnt, long long* Hcnt, PrepStats* st) {
+// Edge-parallel split.  Each warp streams one contiguous, equal-sized range
+// of the input edge array (coalesced 32-edge windows, so hub rows and runs of
+// short rows cost the same per edge); every lane tracks the input row of its
+// edge by walking indptr forward.  Input row v becomes output row perm[v]
+// (identity when perm == nullptr) and columns are renamed through perm -- the
+// solver's degree-sorted relabeling.  Predicates exactly as split_edges
+// (sssp.py:96-97): light 0 < w <= delta, heavy delta < w < inf, in f64.
+
+__device__ __forceinline__ long long warp_first_row(const long long* indptr, long long n,
+                                                    long long e) {
+    // largest r with indptr[r] <= e (indptr[r + 1] > e since e < nnz)
+    long long lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const long long mid = (lo + hi) >> 1;
+        if (__ldg(indptr + mid) <= e) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// per-row light/heavy counts in INPUT order (cL/cH zeroed by the caller;
+// rows cut by a window or warp boundary add their pieces atomically), the
+// minimum light weight, largest weight and fixed-point fraction bits
+__global__ void k_split_count(long long nnz, long long n, const long long* indptr, const double* w,
+                              double delta, unsigned* cL, unsigned* cH, PrepStats* st) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long per = ((nnz + nwarps - 1) / nwarps + 31) & ~31LL;
+    const long long e_begin = warp * per, e_end = min(nnz, e_begin + per);
     unsigned long long minL = ~0ull, maxw = 0, nl = 0, nh = 0;
     int frac = 0;
-    for (long long v = warp; v < n; v += nwarps) {
-        const long long a = indptr[v], b = indptr[v + 1];
-        const long long r = perm ? perm[v] : v;
-        unsigned lc = 0, hc = 0;
-        for (long long e = a + lane; e < b; e += 32) {
-            const double x = __ldg(w + e);
-            const bool L = light_w(x, delta), H = heavy_w(x, delta);
-            lc += L;
-            hc += H;
-            if (L || H) {
-                const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-                if (L && bits < minL) minL = bits;
-                if (bits > maxw) maxw = bits;
-                frac = max(frac, frac_bits(x));
+    if (e_begin < e_end) {
+        long long r = warp_first_row(indptr, n, e_begin);
+        for (long long e0 = e_begin; e0 < e_end; e0 += 32) {
+            const long long e = e0 + lane;
+            const bool valid = e < e_end;
+            bool L = false, H = false;
+            if (valid) {
+                while (__ldg(indptr + r + 1) <= e) ++r;
+                const double x = __ldg(w + e);
+                L = light_w(x, delta);
+                H = heavy_w(x, delta);
+                if (L || H) {
+                    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+                    if (L && bits < minL) minL = bits;
+                    if (bits > maxw) maxw = bits;
+                    frac = max(frac, frac_bits(x));
+                }
             }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            lc += __shfl_xor_sync(0xffffffffu, lc, o);
-            hc += __shfl_xor_sync(0xffffffffu, hc, o);
-        }
-        if (lane == 0) {
-            Lcnt[r] = lc;
-            Hcnt[r] = hc;
-            nl += lc;
-            nh += hc;
+            const unsigned bl = __ballot_sync(0xffffffffu, L), bh = __ballot_sync(0xffffffffu, H);
+            const unsigned peers = __match_any_sync(0xffffffffu, valid ? r : -1LL);
+            if (valid && lane == __ffs(peers) - 1) {
+                const unsigned lc = __popc(peers & bl), hc = __popc(peers & bh);
+                if (lc) atomicAdd(cL + r, lc);
+                if (hc) atomicAdd(cH + r, hc);
+            }
+            if (lane == 0) {
+                nl += __popc(bl);
+                nh += __popc(bh);
+            }
         }
     }
     minL = warp_min(minL);
     maxw = warp_max(maxw);
-    nl = warp_sum(nl);
-    nh = warp_sum(nh);
 #pragma unroll
     for (int o = 16; o; o >>= 1) frac = max(frac, __shfl_xor_sync(0xffffffffu, frac, o));
     if (lane == 0) {
@@ -456,6 +478,17 @@ __global__ void k_split_count(long long n, const long long* indptr, const double
         if (frac) atomicMax(&st->max_frac, frac);
         if (nl) atomicAdd(&st->nL, nl);
         if (nh) atomicAdd(&st->nH, nh);
+    }
+}
+
+// output-order counts for the offset scans: Lcnt[i] = cL[order[i]]
+__global__ void k_gather_counts(long long n, const int* order, const unsigned* cL,
+                                const unsigned* cH, long long* Lcnt, long long* Hcnt) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long v = order ? order[i] : i;
+        Lcnt[i] = cL[v];
+        Hcnt[i] = cH[v];
     }
 }
 
@@ -470,39 +503,80 @@ __device__ __forceinline__ void put_edge(EdgeF64* out, long long i, int c, doubl
     out[i] = e;
 }
 
-// warp per row: stable partition of the row into A_L / A_H (order preserved,
-// filter_matrix semantics, ops.py:158-176)
+// Stable partition of every row into A_L / A_H (order preserved,
+// filter_matrix semantics, ops.py:158-176), same warp ranges as the count.
+// An edge's rank inside its row's light (heavy) part is the warp's running
+// light (heavy) count at the edge minus the count at the row's first edge;
+// only the row that continues from the previous window carries its head
+// count, every other row starts inside the window (its lowest lane).
 template <class Edge>
-__global__ void k_split_scatter(long long n, const long long* indptr, const int* col,
+__global__ void k_split_scatter(long long nnz, long long n, const long long* indptr, const int* col,
                                 const double* w, double delta, int frac, const int* perm,
                                 const long long* Lptr, const long long* Hptr, Edge* Lout,
                                 Edge* Hout) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long per = ((nnz + nwarps - 1) / nwarps + 31) & ~31LL;
+    const long long e_begin = warp * per, e_end = min(nnz, e_begin + per);
+    if (e_begin >= e_end) return;
     const unsigned lt = (1u << lane) - 1u;
-    for (long long v = warp; v < n; v += nwarps) {
-        const long long a = indptr[v], b = indptr[v + 1];
-        const long long r = perm ? perm[v] : v;
-        long long lb = Lptr[r], hb = Hptr[r];
-        for (long long e0 = a; e0 < b; e0 += 32) {
-            const long long e = e0 + lane;
-            double x = 0;
-            int c = 0;
-            if (e < b) {
-                x = __ldg(w + e);
-                c = __ldg(col + e);
-                if (perm) c = __ldg(perm + c);
-            }
-            const bool L = e < b && light_w(x, delta);
-            const bool H = e < b && heavy_w(x, delta);
-            const unsigned mL = __ballot_sync(0xffffffffu, L);
-            const unsigned mH = __ballot_sync(0xffffffffu, H);
-            if (L) put_edge(Lout, lb + __popc(mL & lt), c, x, frac);
-            if (H) put_edge(Hout, hb + __popc(mH & lt), c, x, frac);
-            lb += __popc(mL);
-            hb += __popc(mH);
+    long long r = warp_first_row(indptr, n, e_begin);
+    // the first row may have started in an earlier warp's range: count its
+    // light / heavy edges before e_begin
+    long long preL = 0, preH = 0;
+    for (long long e = __ldg(indptr + r) + lane; e < e_begin; e += 32) {
+        const double x = __ldg(w + e);
+        preL += light_w(x, delta);
+        preH += heavy_w(x, delta);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        preL += __shfl_xor_sync(0xffffffffu, preL, o);
+        preH += __shfl_xor_sync(0xffffffffu, preH, o);
+    }
+    long long carry_r = r, carry_hL = -preL, carry_hH = -preH;
+    long long wl = 0, wh = 0;  // light / heavy edges of this warp before the window
+    long long cur_r = -1, baseL = 0, baseH = 0;
+    for (long long e0 = e_begin; e0 < e_end; e0 += 32) {
+        const long long e = e0 + lane;
+        const bool valid = e < e_end;
+        double x = 0;
+        int c = 0;
+        if (valid) {
+            while (__ldg(indptr + r + 1) <= e) ++r;
+            x = __ldg(w + e);
+            c = __ldg(col + e);
+            if (perm) c = __ldg(perm + c);
         }
+        const bool L = valid && light_w(x, delta);
+        const bool H = valid && heavy_w(x, delta);
+        const unsigned bl = __ballot_sync(0xffffffffu, L), bh = __ballot_sync(0xffffffffu, H);
+        const long long pl = wl + __popc(bl & lt), ph = wh + __popc(bh & lt);
+        const unsigned peers = __match_any_sync(0xffffffffu, valid ? r : -1LL);
+        const int leader = __ffs(peers) - 1;
+        long long hL = __shfl_sync(0xffffffffu, pl, leader);
+        long long hH = __shfl_sync(0xffffffffu, ph, leader);
+        if (r == carry_r) {
+            hL = carry_hL;
+            hH = carry_hH;
+        }
+        if (L || H) {
+            if (r != cur_r) {
+                cur_r = r;
+                const long long o = perm ? perm[r] : r;
+                baseL = Lptr[o];
+                baseH = Hptr[o];
+            }
+            if (L) put_edge(Lout, baseL + (pl - hL), c, x, frac);
+            if (H) put_edge(Hout, baseH + (ph - hH), c, x, frac);
+        }
+        // the row of the window's last edge may continue into the next window
+        carry_r = __shfl_sync(0xffffffffu, r, 31);
+        carry_hL = __shfl_sync(0xffffffffu, hL, 31);
+        carry_hH = __shfl_sync(0xffffffffu, hH, 31);
+        wl += __popc(bl);
+        wh += __popc(bh);
     }
 }
 
@@ -1081,6 +1155,22 @@ static int ensure_edges(void** buf, size_t* cap, size_t bytes) {
     return DS_OK;
 }
 
+// per-row light / heavy counts in output order into Rpre / Rbase (the
+// relabeled order when `relabel`, else input order), stats into `st`
+static int split_counts(ds_graph* g, double delta, bool relabel, PrepStats* st) {
+    unsigned* cL = reinterpret_cast<unsigned*>(g->Rd);  // 2n u32 of scratch
+    unsigned* cH = cL + g->n;
+    CK(cudaMemsetAsync(cL, 0, sizeof(unsigned) * 2 * (size_t)g->n, g->stream));
+    if (g->nnz > 0)
+        k_split_count<<<(unsigned)(g->nsm * 16), 256, 0, g->stream>>>(g->nnz, g->n, g->indptr, g->w,
+                                                                     delta, cL, cH, st);
+    CK(cudaGetLastError());
+    k_gather_counts<<<elementwise_grid(g), 256, 0, g->stream>>>(g->n, relabel ? g->order : nullptr,
+                                                                 cL, cH, g->Rpre, g->Rbase);
+    CK(cudaGetLastError());
+    return DS_OK;
+}
+
 static int prepare(ds_graph* g, double delta, uint32_t flags) {
     if (!(delta > 0) || !std::isfinite(delta))
         return set_err(DS_EINVAL, "delta must be a positive finite number, got %g", delta);
@@ -1098,10 +1188,9 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     CK(cudaMemsetAsync(g->Hptr, 0, sizeof(long long), g->stream));
     // per-row counts into scratch (Rpre / Rbase are n-sized int64)
     const unsigned grid = (unsigned)(g->nsm * 16);
-    k_split_count<<<grid, 256, 0, g->stream>>>(n, g->indptr, g->w, delta, g->perm, g->Rpre, g->Rbase,
-                                               g->pstat);
-    CK(cudaGetLastError());
-    int rc = inclusive_scan_i64(g, g->Rpre, g->Lptr + 1, n);
+    int rc = split_counts(g, delta, true, g->pstat);
+    if (rc) return rc;
+    rc = inclusive_scan_i64(g, g->Rpre, g->Lptr + 1, n);
     if (rc) return rc;
     rc = inclusive_scan_i64(g, g->Rbase, g->Hptr + 1, n);
     if (rc) return rc;
@@ -1137,11 +1226,11 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     if ((rc = ensure_edges(&g->Ledges, &g->Lcap, esz * (size_t)g->nL))) return rc;
     if ((rc = ensure_edges(&g->Hedges, &g->Hcap, esz * (size_t)g->nH))) return rc;
     if (mode == DS_MODE_FIXED32)
-        k_split_scatter<uint2><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, delta, g->frac,
+        k_split_scatter<uint2><<<grid, 256, 0, g->stream>>>(g->nnz, n, g->indptr, g->col, g->w, delta, g->frac,
                                                             g->perm, g->Lptr, g->Hptr,
                                                             (uint2*)g->Ledges, (uint2*)g->Hedges);
     else
-        k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, delta, 0,
+        k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(g->nnz, n, g->indptr, g->col, g->w, delta, 0,
                                                               g->perm, g->Lptr, g->Hptr,
                                                               (EdgeF64*)g->Ledges,
                                                               (EdgeF64*)g->Hedges);
@@ -1674,12 +1763,10 @@ extern "C" int ds_export_split(ds_graph* g, int which, int64_t* indptr, int64_t*
     PrepStats* st = g->pstat;
     CKE(cudaMemsetAsync(st, 0, sizeof(PrepStats), g->stream));
     const unsigned grid = (unsigned)(g->nsm * 16);
-    k_split_count<<<grid, 256, 0, g->stream>>>(n, g->indptr, g->w, g->delta, nullptr, g->Rpre,
-                                               g->Rbase, st);
-    CKE(cudaGetLastError());
+    if ((rc = split_counts(g, g->delta, false, st))) return done(rc);
     if ((rc = inclusive_scan_i64(g, g->Rpre, ptrL + 1, n))) return done(rc);
     if ((rc = inclusive_scan_i64(g, g->Rbase, ptrH + 1, n))) return done(rc);
-    k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(n, g->indptr, g->col, g->w, g->delta, 0,
+    k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(g->nnz, n, g->indptr, g->col, g->w, g->delta, 0,
                                                           nullptr, ptrL, ptrH, eL, eH);
     CKE(cudaGetLastError());
     CKE(cudaMemcpyAsync(indptr, which ? ptrH : ptrL, sizeof(long long) * (n + 1), cudaMemcpyDefault,
