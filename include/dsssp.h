@@ -44,6 +44,8 @@ extern "C" {
 #define DS_ECUDA 3
 #define DS_ENOMEM 4
 #define DS_ETIMEOUT 5
+#define DS_EPARSE 6  /* graph file structure -> deltasparse.io.ParseError      */
+#define DS_EVALID 7  /* graph file content   -> deltasparse.io.ValidationError */
 
 /* column-index dtypes */
 #define DS_IDX_I32 0
@@ -186,6 +188,28 @@ int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const uint64_t* v
 int ds_shard_result(ds_shard* s, double* out);
 /* Shard [v0, v1) cut on the device from a resident graph handle. */
 int ds_shard_from_graph(ds_graph* g, int64_t v0, int64_t v1, ds_shard** out);
+
+/* ---- graph-file ingestion (host side, no device needed) -----------------
+ * Native parser for the reference loaders (deltasparse/io.py):
+ *   DS_FMT_MTX   <- load_matrix_market(path, default_weight)   io.py:121-193
+ *   DS_FMT_EDGES <- load_edge_list(path, directed, default_weight) io.py:196-259
+ * over an in-memory file image (`name` is used in messages only).  Errors
+ * read "name:lineno: message" (ds_last_error) with the line number also in
+ * ds_ingest_error_line(); DS_EPARSE / DS_EVALID mirror ParseError /
+ * ValidationError.  The result is the COO entry list in file order (mirrored
+ * for symmetric / undirected input, self-loops dropped and counted) and the
+ * external label of every internal id; build the CSR with matrix_build
+ * semantics (duplicates keep the minimum weight, core.py:247-278). */
+#define DS_FMT_MTX 0
+#define DS_FMT_EDGES 1
+typedef struct ds_ingest ds_ingest;
+int ds_ingest_parse(const char* data, int64_t len, int32_t format, int32_t directed,
+                    double default_weight, const char* name, ds_ingest** out);
+int ds_ingest_info(const ds_ingest* h, int64_t* n, int64_t* entries, int64_t* self_loops);
+/* rows/cols/vals: `entries` each; labels: n (any may be NULL) */
+int ds_ingest_copy(const ds_ingest* h, int64_t* rows, int64_t* cols, double* vals, int64_t* labels);
+int64_t ds_ingest_error_line(void);
+void ds_ingest_free(ds_ingest* h);
 
 #ifdef __cplusplus
 }

@@ -3,7 +3,9 @@
 Public names follow the reference package `deltasparse` for this path
 (/root/reference/pkg/src/deltasparse/__init__.py): `delta_stepping`,
 `SsspResult`, `split_edges`, `BackendChoice`, `bucket_bounds`, the
-`SparseMatrix` / `SparseVector` containers and their builders.  Compute runs
+`SparseMatrix` / `SparseVector` containers and their builders, and the graph
+file loaders (`load_matrix_market`, `load_edge_list`, `load_graph`, parsed
+natively).  Compute runs
 in libdsssp.so (sm_100a) through the C-ABI declared in include/dsssp.h.
 """
 
@@ -15,6 +17,16 @@ from .containers import (  # noqa: F401
     vector_build,
 )
 from .graphs import random_connected_unit_graph, random_graph  # noqa: F401
+from .io import (  # noqa: F401
+    GraphFile,
+    GraphLoadError,
+    LabelMap,
+    ParseError,
+    ValidationError,
+    load_edge_list,
+    load_graph,
+    load_matrix_market,
+)
 from .sssp import (  # noqa: F401
     BackendChoice,
     DeviceGraph,
@@ -44,5 +56,13 @@ __all__ = [
     "delta_stepping",
     "delta_stepping_batch",
     "split_edges",
+    "GraphFile",
+    "GraphLoadError",
+    "LabelMap",
+    "ParseError",
+    "ValidationError",
+    "load_edge_list",
+    "load_graph",
+    "load_matrix_market",
     "__version__",
 ]

@@ -13,6 +13,8 @@ import threading
 from .build import LIB
 
 DS_OK, DS_EINVAL, DS_ENOCONVERGE, DS_ECUDA, DS_ENOMEM, DS_ETIMEOUT = 0, 1, 2, 3, 4, 5
+DS_EPARSE, DS_EVALID = 6, 7
+DS_FMT_MTX, DS_FMT_EDGES = 0, 1
 DS_IDX_I32, DS_IDX_I64 = 0, 1
 DS_W_F32, DS_W_F64, DS_W_I32 = 0, 1, 2
 DS_FLAG_SKIP_EMPTY, DS_FLAG_FORCE_F64 = 1, 2
@@ -26,7 +28,8 @@ EXPORTS = (
     "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download", "ds_debug_trace",
     "ds_shard_create", "ds_shard_destroy", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",
     "ds_shard_scan", "ds_shard_s_add", "ds_shard_relax", "ds_shard_result", "ds_shard_from_graph",
-    "ds_release_pool",
+    "ds_release_pool", "ds_ingest_parse", "ds_ingest_info", "ds_ingest_copy",
+    "ds_ingest_error_line", "ds_ingest_free",
 )
 
 
@@ -98,6 +101,14 @@ def lib():
         L.ds_sssp.argtypes = [_vp, _i64, ctypes.c_double, ctypes.c_uint32, ctypes.POINTER(Stats)]
         L.ds_sssp_batch.argtypes = [_vp, _vp, _i64, ctypes.c_double, ctypes.c_uint32, ctypes.c_int32,
                                     _vp, _vp]
+        L.ds_ingest_parse.argtypes = [ctypes.c_char_p, _i64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                      ctypes.c_char_p, ctypes.POINTER(_vp)]
+        L.ds_ingest_info.argtypes = [_vp, _i64p, _i64p, _i64p]
+        L.ds_ingest_copy.argtypes = [_vp, _vp, _vp, _vp, _vp]
+        L.ds_ingest_error_line.restype = ctypes.c_int64
+        L.ds_ingest_error_line.argtypes = []
+        L.ds_ingest_free.restype = None
+        L.ds_ingest_free.argtypes = [_vp]
         L.ds_result_dense.argtypes = [_vp, _vp]
         L.ds_result_sparse.argtypes = [_vp, _vp, _vp]
         L.ds_export_split.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp]

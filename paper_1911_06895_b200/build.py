@@ -21,7 +21,7 @@ LIB = os.path.join(LIB_DIR, "libdsssp.so")
 # variant with the pull (vxm) relaxations compiled in (opt-in)
 LIB_PULL = os.path.join(LIB_DIR, "libdsssp_pull.so")
 VARIANTS = {LIB: [], LIB_PULL: ["-DDS_PULL_LIGHT=1", "-DDS_PULL_HEAVY=1"]}
-SOURCES = ["dsssp.cu", "gen.cu", "shard.cu"]
+SOURCES = ["dsssp.cu", "gen.cu", "shard.cu", "ingest.cpp"]
 HEADERS = ["common.cuh", "sssp_kernel.cuh"]
 
 NVCC_FLAGS = [

@@ -151,6 +151,9 @@ constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 #ifndef DS_PULL_HEAVY
 #define DS_PULL_HEAVY 0
 #endif
+#ifndef DS_PIPE
+#define DS_PIPE 0  // software-pipelined push: next chunk's entries load under this chunk's edges
+#endif
 
 struct StepSlot {
     unsigned long long re_packed;     // capture: reserved (entries << 33) | edges
@@ -251,8 +254,21 @@ struct WarpSmem {
     int rel[kChunk + 1];
     unsigned short row[kChunk];
     int q[kQueue];
-    D qv[kQueue];
+#if DS_PULL_LIGHT || DS_PULL_HEAVY
+    D qv[kQueue];  // values travelling with pull-produced lists
+#endif
+#if DS_PIPE
+    D du[kChunk];  // pipelined push: per-edge source value of the chunk in flight
+#endif
 };
+template <class D>
+__device__ __forceinline__ D* queue_vals(WarpSmem<D>& ws) {
+#if DS_PULL_LIGHT || DS_PULL_HEAVY
+    return ws.qv;
+#else
+    return nullptr;
+#endif
+}
 
 template <class D>
 struct Smem {
@@ -563,10 +579,10 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
             }
 #pragma unroll
             for (int j = 0; j < kListPer; ++j)
-                wq_push<D, false>(ws.q, ws.qv, qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
+                wq_push<D, false>(ws.q, queue_vals(ws), qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
             capture_emit<M, kListPer>(p, slot, lane, cd, off, deg);
         }
-        wq_flush<D, false>(ws.q, ws.qv, qn, lane, S, nullptr, s_counter);
+        wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
     }
     const unsigned long long fc = block_reduce<0>(local_fc, sm.red);
     const unsigned long long mn = block_reduce<1>(local_min, sm.red2);
@@ -623,8 +639,8 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
             for (int j = 0; j < kListPer; ++j) news[j] = in[j] && claim_bit(p.sbits, (unsigned)vtx[j]);
 #pragma unroll
             for (int j = 0; j < kListPer; ++j)
-                wq_push<D, false>(ws.q, ws.qv, qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
-            wq_flush<D, false>(ws.q, ws.qv, qn, lane, S, nullptr, s_counter);
+                wq_push<D, false>(ws.q, queue_vals(ws), qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
+            wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
         }
         capture_emit<M, kListPer>(p, slot, lane, dv, off, deg);
     }
@@ -656,7 +672,9 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     const unsigned long long nw = LOCALW ? kWarps : (unsigned long long)gridDim.x * kWarps;
     const unsigned long long pol = LIGHT ? light_policy() : evict_first_policy();
     bool overflow = false;
-    for (unsigned long long c = gw; c < nchunk; c += nw) {
+    // entries of chunk c -> this warp's smem (offset, row base, captured d)
+    // and the row map: lane resolves the entry of chunk edges [8 lane, 8 lane + 8)
+    auto load_meta = [&](unsigned long long c) {
         const unsigned long long r0 = ldcg(p.chunk_start + c);
         const unsigned long long r1 = (c + 1 < nchunk) ? ldcg(p.chunk_start + c + 1) : Rc - 1;
         const int ne = (int)(r1 - r0 + 1);
@@ -669,42 +687,65 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             ws.d[k] = __ldcg(p.Rd + r);
         }
         __syncwarp();
-        {   // row map: lane resolves the entry of chunk edges [8 lane, 8 lane + 8)
-            const int rel0 = lane * kRelPer;
-            int lo = 0, hi = ne;
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (ws.rel[mid] <= rel0) lo = mid;
-                else hi = mid;
-            }
-            int k = lo;
+        const int rel0 = lane * kRelPer;
+        int lo = 0, hi = ne;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (ws.rel[mid] <= rel0) lo = mid;
+            else hi = mid;
+        }
+        int k = lo;
 #pragma unroll
-            for (int j = 0; j < kRelPer; ++j) {
-                while (k + 1 < ne && ws.rel[k + 1] <= rel0 + j) ++k;
-                ws.row[rel0 + j] = (unsigned short)k;
-            }
+        for (int j = 0; j < kRelPer; ++j) {
+            while (k + 1 < ne && ws.rel[k + 1] <= rel0 + j) ++k;
+            ws.row[rel0 + j] = (unsigned short)k;
         }
         __syncwarp();
+    };
+#if DS_PIPE
+    if (gw < nchunk) load_meta(gw);
+#endif
+    for (unsigned long long c = gw; c < nchunk; c += nw) {
+        const long long cb = (long long)(c * kChunk);
+#if !DS_PIPE
+        load_meta(c);
+#endif
         const long long left = (long long)E - cb - lane;  // edge j exists iff 32 j < left
-        int kk[kRelPer];
         Edge ed[kRelPer];
+#if DS_PIPE
+        // issue this chunk's edge loads, park the per-edge source values in
+        // smem, then fetch the next chunk's entries while the edges are in flight
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j) {
+            const int r = lane + 32 * j;
+            const int kj = ws.row[r];
+            if (32 * j < left) ed[j] = M::load(edges + (ws.base[kj] + cb + r), pol);
+            ws.du[r] = ws.d[kj];
+        }
+        __syncwarp();
+        if (c + nw < nchunk) load_meta(c + nw);
+#define DS_DU(j) ws.du[lane + 32 * (j)]
+#else
+        int kk[kRelPer];
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             const int r = lane + 32 * j;
             kk[j] = ws.row[r];
             if (32 * j < left) ed[j] = M::load(edges + (ws.base[kk[j]] + cb + r), pol);
         }
+#define DS_DU(j) ws.d[kk[j]]
+#endif
         D nd[kRelPer], cur[kRelPer];
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             cur[j] = (D)0;
             if (32 * j < left) {
-                if (M::add(ws.d[kk[j]], ed[j], nd[j])) {
+                if (M::add(DS_DU(j), ed[j], nd[j])) {
                     // a stale (L1) value is >= the current one: it can only
                     // cause a redundant atomic, never a missed improvement
-                    cur[j] = (LIGHT || !kHeavyRed)
-                                 ? (DS_PRECHECK_L1 ? p.dist[M::col(ed[j])] : __ldcg(p.dist + M::col(ed[j])))
-                                 : M::INF;
+                    const unsigned v = M::col(ed[j]);
+                    cur[j] = (LIGHT || !kHeavyRed) ? (DS_PRECHECK_L1 ? p.dist[v] : __ldcg(p.dist + v))
+                                                   : M::INF;
                 } else {
                     overflow = true;
                 }
@@ -732,15 +773,16 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             }
 #pragma unroll
             for (int j = 0; j < kRelPer; ++j)
-                wq_push<D, false>(ws.q, ws.qv, qn, got[j] != 0, (int)M::col(ed[j]), (D)0, lane,
+                wq_push<D, false>(ws.q, queue_vals(ws), qn, got[j] != 0, (int)M::col(ed[j]), (D)0, lane,
                                   out_list, nullptr, &slot->append_count);
-            wq_flush<D, false>(ws.q, ws.qv, qn, lane, out_list, nullptr, &slot->append_count);
+            wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
         } else {
 #pragma unroll
             for (int j = 0; j < kRelPer; ++j)
                 if (32 * j < left && nd[j] < cur[j]) atomicMin(p.dist + M::col(ed[j]), nd[j]);
         }
         __syncwarp();
+#undef DS_DU
     }
     if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, 1u);
 }
@@ -880,10 +922,10 @@ __device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot
                 }
             }
             if (LIGHT)
-                wq_push<D, true>(ws.q, ws.qv, qn, want, rr, val, lane, out_list, out_vals,
+                wq_push<D, true>(ws.q, queue_vals(ws), qn, want, rr, val, lane, out_list, out_vals,
                                  &slot->append_count);
         }
-        if (LIGHT) wq_flush<D, true>(ws.q, ws.qv, qn, lane, out_list, out_vals, &slot->append_count);
+        if (LIGHT) wq_flush<D, true>(ws.q, queue_vals(ws), qn, lane, out_list, out_vals, &slot->append_count);
         __syncwarp();
     }
     if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, 1u);
@@ -922,10 +964,10 @@ __device__ void commit_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSl
             }
         }
         if (LIGHT)
-            wq_push<D, true>(ws.q, ws.qv, qn, want, rr, val, lane, out_list, out_vals,
+            wq_push<D, true>(ws.q, queue_vals(ws), qn, want, rr, val, lane, out_list, out_vals,
                              &slot->append_count);
     }
-    if (LIGHT) wq_flush<D, true>(ws.q, ws.qv, qn, lane, out_list, out_vals, &slot->append_count);
+    if (LIGHT) wq_flush<D, true>(ws.q, queue_vals(ws), qn, lane, out_list, out_vals, &slot->append_count);
 }
 
 // ---------------------------------------------------------------- the solver
