@@ -348,6 +348,9 @@ static bool is_device_ptr(const void* p) {
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// dynamic shared memory of the standalone push: the per-warp areas it uses
+static int big_smem(size_t warp_bytes) { return (int)(warp_bytes * (kBigThreads / 32)); }
+
 static unsigned grid_blocks_for(int nsm, int occ) {
     int per = std::max(1, std::min(occ, 8));
     if (const char* s = getenv("DS_BLOCKS_PER_SM")) per = std::max(1, std::min(per, atoi(s)));
@@ -866,9 +869,10 @@ static int alloc_scratch(ds_graph* g) {
         CK(cudaFuncSetAttribute(k_big_relax<ModeF64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s6));
         CK(cudaFuncSetAttribute(k_big_relax<ModeF64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s6));
         int o = 1;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_big_relax<ModeFixed, true>, kThreads, sf));
+        const int bs = big_smem(sizeof(WarpSmem<unsigned>));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_big_relax<ModeFixed, true>, kBigThreads, bs));
         g->occ_big_l = std::max(o, 1);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_big_relax<ModeFixed, false>, kThreads, sf));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_big_relax<ModeFixed, false>, kBigThreads, bs));
         g->occ_big_h = std::max(o, 1);
     }
     if (g->grid_fixed <= 0 || g->grid_f64 <= 0)
@@ -1374,7 +1378,6 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     // The persistent kernel runs the whole solve on the device; it only stops
     // to hand a giant push to k_big_relax (its own launch and register
     // budget), after which it is relaunched and resumes from Ctl.
-    const size_t smem = sizeof(Smem<typename M::D>);
     x.launches = 0;
     for (int hop = 0;; ++hop) {
         ++x.launches;
@@ -1388,10 +1391,11 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         if (h.abort || h.status != 0 || h.rs_req == 0) break;
         const unsigned rgrid = (unsigned)(g->nsm * (h.rs_req == 1 ? g->occ_big_l : g->occ_big_h));
         ++x.launches;
+        const int bsm = big_smem(sizeof(WarpSmem<typename M::D>));
         if (h.rs_req == 1)
-            k_big_relax<M, true><<<rgrid, kThreads, smem, x.stream>>>(p);
+            k_big_relax<M, true><<<rgrid, kBigThreads, bsm, x.stream>>>(p);
         else
-            k_big_relax<M, false><<<rgrid, kThreads, smem, x.stream>>>(p);
+            k_big_relax<M, false><<<rgrid, kBigThreads, bsm, x.stream>>>(p);
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(x.ev1, x.stream));

@@ -126,6 +126,15 @@ struct ModeF64 {
 constexpr int kPackShift = 33;  // capture reservation: (entries << 33) | edges
 constexpr unsigned long long kMask33 = (1ull << kPackShift) - 1;
 constexpr int kWarps = kThreads / 32;
+// standalone giant-push kernel: its own block shape (uses Smem::w[0 .. warps))
+#ifndef DS_BIG_THREADS
+#define DS_BIG_THREADS DS_THREADS
+#endif
+#ifndef DS_BIG_MINB
+#define DS_BIG_MINB 1
+#endif
+constexpr int kBigThreads = DS_BIG_THREADS;
+static_assert(kBigThreads % 32 == 0 && kBigThreads <= kThreads, "standalone push block shape");
 #ifndef DS_CHUNK
 #define DS_CHUNK 256
 #endif
@@ -668,8 +677,10 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     WarpSmem<D>& ws = sm.w[wib];
     unsigned qn = 0;
     const unsigned long long nchunk = (E + kChunk - 1) / kChunk;
-    const unsigned long long gw = LOCALW ? wib : (unsigned long long)blockIdx.x * kWarps + wib;
-    const unsigned long long nw = LOCALW ? kWarps : (unsigned long long)gridDim.x * kWarps;
+    // warps per block from the launch: the standalone push may run narrower blocks
+    const unsigned wpb = LOCALW ? (unsigned)kWarps : (blockDim.x >> 5);
+    const unsigned long long gw = LOCALW ? wib : (unsigned long long)blockIdx.x * wpb + wib;
+    const unsigned long long nw = LOCALW ? kWarps : (unsigned long long)gridDim.x * wpb;
     const unsigned long long pol = LIGHT ? light_policy() : evict_first_policy();
     bool overflow = false;
     // entries of chunk c -> this warp's smem (offset, row base, captured d)
@@ -1402,7 +1413,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
 // own register allocation, no spills): the solver state says which list,
 // window and CSR; results land in Ctl::xslot.
 template <class M, bool LIGHT>
-__global__ void __launch_bounds__(kThreads) k_big_relax(const KParams<M> p) {
+__global__ void __launch_bounds__(kBigThreads, DS_BIG_MINB) k_big_relax(const KParams<M> p) {
     using D = typename M::D;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
