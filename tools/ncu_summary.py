@@ -31,7 +31,7 @@ for r in data:
         "dram_read": f(r, "dram__bytes_read.sum"),
         "dram_write": f(r, "dram__bytes_write.sum"),
         "l2_hit_pct": f(r, "lts__t_sector_hit_rate.pct"),
-        "dram_pct": f(r, "dram__throughput.avg.pct_of_peak_sustained_elapsed"),
+        "dram_pct": f(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
         "warps_active_pct": f(r, "sm__warps_active.avg.pct_of_peak_sustained_active"),
         "registers": f(r, "launch__registers_per_thread"),
     })
