@@ -160,6 +160,12 @@ constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 #ifndef DS_PULL_HEAVY
 #define DS_PULL_HEAVY 0
 #endif
+#ifndef DS_BARRIER
+#define DS_BARRIER 1  // 1: monotonic-counter grid barrier (0: counter + generation pair)
+#endif
+#ifndef DS_BARRIER_SLEEP
+#define DS_BARRIER_SLEEP 0
+#endif
 #ifndef DS_PIPE
 #define DS_PIPE 0  // software-pipelined push: next chunk's entries load under this chunk's edges
 #endif
@@ -177,6 +183,7 @@ struct StepSlot {
 struct Ctl {
     unsigned bar_count;
     unsigned bar_gen;
+    unsigned long long bar_arrive;  // DS_BARRIER=1: monotonic arrival counter
     unsigned abort;
     int status;  // DS_* code raised on the device
     StepSlot slot[3];
@@ -371,6 +378,39 @@ template <class S>
 __device__ __forceinline__ bool grid_sync(Ctl* c, unsigned& gen, unsigned long long deadline,
                                           S& sm) {
     __syncthreads();
+#if DS_BARRIER == 1
+    // monotonic counter: arrive with a fire-and-forget release add, wait until
+    // every CTA's arrival for this generation is visible (no reset, no second
+    // release store, one round trip less than the counter + generation pair)
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        const unsigned long long target = (unsigned long long)(gen + 1) * gridDim.x;
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(&c->bar_arrive) : "memory");
+        unsigned spins = 0;
+        while (ld_acquire_u64(&c->bar_arrive) < target) {
+#if DS_BARRIER_SLEEP
+            __nanosleep(DS_BARRIER_SLEEP);
+#endif
+            if ((++spins & 1023u) == 0) {
+                if (ld_acquire_u32(&c->abort)) {
+                    ok = 0;
+                    break;
+                }
+                if (globaltimer_ns() > deadline) {
+                    atomicExch(&c->abort, 1u);
+                    ok = 0;
+                    break;
+                }
+            }
+        }
+        __threadfence();
+        gen += 1;
+        if (ld_acquire_u32(&c->abort)) ok = 0;
+        sm.ok = ok;
+    }
+    __syncthreads();
+    return sm.ok != 0;
+#else
     if (threadIdx.x == 0) {
         int ok = 1;
         const unsigned target = gen + 1;
@@ -402,6 +442,7 @@ __device__ __forceinline__ bool grid_sync(Ctl* c, unsigned& gen, unsigned long l
     }
     __syncthreads();
     return sm.ok != 0;
+#endif
 }
 
 // Warp-uniform append: every lane calls it; lanes with `want` land in the
@@ -995,7 +1036,12 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     const int pos0 = (int)ldcg(&c->rs_pos);
     if (threadIdx.x == 0) {
         deadline = globaltimer_ns() + p.timeout_ns;
-        gen = ldcg(&c->bar_gen);  // resumed launches continue the barrier sequence
+        // resumed launches continue the barrier sequence
+#if DS_BARRIER == 1
+        gen = (unsigned)(ldcg(&c->bar_arrive) / gridDim.x);
+#else
+        gen = ldcg(&c->bar_gen);
+#endif
     }
 
     // ---- init: t = {source: 0} (sssp.py:276), all else +inf.  Only solver
