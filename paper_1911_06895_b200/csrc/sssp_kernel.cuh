@@ -160,6 +160,9 @@ constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 #ifndef DS_PULL_HEAVY
 #define DS_PULL_HEAVY 0
 #endif
+#ifndef DS_LATE_FLUSH
+#define DS_LATE_FLUSH 1  // 1: flush warp append queues when half full, not per chunk
+#endif
 #ifndef DS_BARRIER
 #define DS_BARRIER 1  // 1: monotonic-counter grid barrier (0: counter + generation pair)
 #endif
@@ -632,8 +635,10 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
                 wq_push<D, false>(ws.q, queue_vals(ws), qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
             capture_emit<M, kListPer>(p, slot, lane, cd, off, deg);
         }
-        wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
+        if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
+            wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
     }
+    wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
     const unsigned long long fc = block_reduce<0>(local_fc, sm.red);
     const unsigned long long mn = block_reduce<1>(local_min, sm.red2);
     if (threadIdx.x == 0) {
@@ -690,10 +695,12 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
 #pragma unroll
             for (int j = 0; j < kListPer; ++j)
                 wq_push<D, false>(ws.q, queue_vals(ws), qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
-            wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
+            if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
+                wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
         }
         capture_emit<M, kListPer>(p, slot, lane, dv, off, deg);
     }
+    if (APPEND_S) wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
 }
 
 // ---------------------------------------------------------------- relax step (push)
@@ -827,7 +834,8 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             for (int j = 0; j < kRelPer; ++j)
                 wq_push<D, false>(ws.q, queue_vals(ws), qn, got[j] != 0, (int)M::col(ed[j]), (D)0, lane,
                                   out_list, nullptr, &slot->append_count);
-            wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
+            if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
+                wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
         } else {
 #pragma unroll
             for (int j = 0; j < kRelPer; ++j)
@@ -836,6 +844,9 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         __syncwarp();
 #undef DS_DU
     }
+    // DS_LATE_FLUSH: appends stay in the warp queue across chunks until it
+    // is half full, so most chunks skip the reservation round trip
+    if (LIGHT) wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
     if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, 1u);
 }
 
