@@ -617,7 +617,11 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
                     const int b = __ffs(rem) - 1;
                     rem &= rem - 1;
                     vtx[j] = (int)(v0 + b);
-                    cd[j] = dv[b];
+                    // select, not dv[b]: a dynamic index would move dv[] to local memory
+                    D x = dv[0];
+#pragma unroll
+                    for (int i = 1; i < kRangePer; ++i) x = (b == i) ? dv[i] : x;
+                    cd[j] = x;
                 }
             }
             bool news[kListPer];
@@ -778,7 +782,9 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         for (int j = 0; j < kRelPer; ++j) {
             const int r = lane + 32 * j;
             const int kj = ws.row[r];
-            if (32 * j < left) ed[j] = M::load(edges + (ws.base[kj] + cb + r), pol);
+            // unconditional definition: a conditionally assigned ed[] is
+            // loop-carried and was spilled to local memory
+            ed[j] = (32 * j < left) ? M::load(edges + (ws.base[kj] + cb + r), pol) : Edge{};
             ws.du[r] = ws.d[kj];
         }
         __syncwarp();
@@ -790,7 +796,9 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         for (int j = 0; j < kRelPer; ++j) {
             const int r = lane + 32 * j;
             kk[j] = ws.row[r];
-            if (32 * j < left) ed[j] = M::load(edges + (ws.base[kk[j]] + cb + r), pol);
+            // unconditional definition: a conditionally assigned ed[] is
+            // loop-carried and was spilled to local memory
+            ed[j] = (32 * j < left) ? M::load(edges + (ws.base[kk[j]] + cb + r), pol) : Edge{};
         }
 #define DS_DU(j) ws.d[kk[j]]
 #endif
