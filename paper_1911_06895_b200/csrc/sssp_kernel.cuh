@@ -806,6 +806,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             cur[j] = (D)0;
+            nd[j] = (D)0;  // defined on every path (see ed[] above)
             if (32 * j < left) {
                 if (M::add(DS_DU(j), ed[j], nd[j])) {
                     // a stale (L1) value is >= the current one: it can only
