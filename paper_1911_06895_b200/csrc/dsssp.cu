@@ -1321,7 +1321,9 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         const char* bl = getenv("DS_BIG_L");
         const char* bh = getenv("DS_BIG_H");
         p.big_light = bl ? (unsigned long long)atoll(bl) : ~0ull;
-        p.big_heavy = bh ? (unsigned long long)atoll(bh) : (4ull << 20);
+        // giant-push handoff off by default: since the push loop stopped
+        // spilling, the in-kernel heavy push is faster than a standalone launch
+        p.big_heavy = bh ? (unsigned long long)atoll(bh) : ~0ull;
         if (grid < full_grid(g)) {
             // concurrent batch contexts: a full-device standalone push would
             // stall the other contexts' grids (measured slower), so no handoff
