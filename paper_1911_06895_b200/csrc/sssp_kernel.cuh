@@ -160,6 +160,9 @@ constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 #ifndef DS_PULL_HEAVY
 #define DS_PULL_HEAVY 0
 #endif
+#ifndef DS_DEFER_APPEND
+#define DS_DEFER_APPEND 1  // 1: consume a chunk's dedup claims after the next chunk's loads
+#endif
 #ifndef DS_LATE_FLUSH
 #define DS_LATE_FLUSH 1  // 1: flush warp append queues when half full, not per chunk
 #endif
@@ -768,6 +771,23 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
 #if DS_PIPE
     if (gw < nchunk) load_meta(gw);
 #endif
+    // DS_DEFER_APPEND (light): a chunk's dedup claims are consumed (appended)
+    // only after the next chunk's edge loads are out, hiding their round trip
+    unsigned p_col[kRelPer], p_ret[kRelPer];
+    unsigned p_req = 0;
+#pragma unroll
+    for (int j = 0; j < kRelPer; ++j) p_col[j] = p_ret[j] = 0u;
+    auto drain = [&]() {
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j) {
+            const bool g = ((p_req >> j) & 1u) && !(p_ret[j] & (1u << (p_col[j] & 31)));
+            wq_push<D, false>(ws.q, queue_vals(ws), qn, g, (int)p_col[j], (D)0, lane, out_list, nullptr,
+                              &slot->append_count);
+        }
+        p_req = 0;
+        if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
+            wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
+    };
     for (unsigned long long c = gw; c < nchunk; c += nw) {
         const long long cb = (long long)(c * kChunk);
 #if !DS_PIPE
@@ -802,6 +822,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         }
 #define DS_DU(j) ws.d[kk[j]]
 #endif
+        if (LIGHT && DS_DEFER_APPEND) drain();  // previous chunk's claims, edges in flight
         D nd[kRelPer], cur[kRelPer];
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
@@ -829,6 +850,16 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                 old[j] = nd[j];
                 if (32 * j < left && nd[j] < cur[j]) old[j] = atomicMin(p.dist + M::col(ed[j]), nd[j]);
             }
+#if DS_DEFER_APPEND
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                const unsigned v = M::col(ed[j]);
+                const bool want = 32 * j < left && nd[j] < old[j] && nd[j] < H;
+                p_col[j] = v;
+                p_ret[j] = want ? atomicOr(fbits + (v >> 5), 1u << (v & 31)) : 0u;
+                p_req |= (want ? 1u : 0u) << j;
+            }
+#else
             unsigned got[kRelPer];
 #pragma unroll
             for (int j = 0; j < kRelPer; ++j) {
@@ -845,6 +876,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                                   out_list, nullptr, &slot->append_count);
             if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
                 wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
+#endif
         } else {
 #pragma unroll
             for (int j = 0; j < kRelPer; ++j)
@@ -853,6 +885,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         __syncwarp();
 #undef DS_DU
     }
+    if (LIGHT && DS_DEFER_APPEND) drain();
     // DS_LATE_FLUSH: appends stay in the warp queue across chunks until it
     // is half full, so most chunks skip the reservation round trip
     if (LIGHT) wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
