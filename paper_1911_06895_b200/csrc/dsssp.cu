@@ -235,6 +235,8 @@ struct ds_graph {
         long long n_nz = 0, nspan = 0, nnz = 0;
     } planL, planH;
     bool symmetric = false;
+    bool sym_checked = false;   // symmetry fingerprint computed (lazily, at the first prepare)
+    bool heavy_plan = false;    // planH valid for the current prepare (standalone heavy pull)
     long long* Rpre = nullptr;
     long long* Rbase = nullptr;
     void* Rd = nullptr;
@@ -868,6 +870,10 @@ static int alloc_scratch(ds_graph* g) {
         CK(cudaFuncSetAttribute(k_big_relax<ModeFixed, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sf));
         CK(cudaFuncSetAttribute(k_big_relax<ModeF64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s6));
         CK(cudaFuncSetAttribute(k_big_relax<ModeF64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s6));
+        CK(cudaFuncSetAttribute(k_big_pull<ModeFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize, sf));
+        CK(cudaFuncSetAttribute(k_big_pull<ModeF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s6));
+        CK(cudaFuncSetAttribute(k_big_commit<ModeFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize, sf));
+        CK(cudaFuncSetAttribute(k_big_commit<ModeF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, s6));
         int o = 1;
         const int bs = big_smem(sizeof(WarpSmem<unsigned>));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_big_relax<ModeFixed, true>, kBigThreads, bs));
@@ -923,6 +929,15 @@ static int check_csr(ds_graph* g) {
     CK(cudaStreamSynchronize(g->stream));
     if (h) return set_err(DS_EINVAL, "indptr must start at 0, be non-decreasing and end at nnz");
     return DS_OK;
+}
+
+// DS_HEAVY_PULL=1 runs giant heavy steps (over half of A_H, or DS_BIG_H) as
+// the standalone gathered step k_big_pull/k_big_commit on symmetric graphs.
+// Measured 2x slower than the in-kernel push on R-MAT 24 (the S-bit gate is a
+// random read per edge of A_H), so it is opt-in; tests keep it exact.
+static bool heavy_pull_wanted() {
+    const char* e = getenv("DS_HEAVY_PULL");
+    return e && atoi(e) != 0;
 }
 
 static int build_plan(ds_graph* g, const long long* ptr, long long nnz, ds_graph::Plan& pl) {
@@ -1243,6 +1258,26 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
         if ((rc = build_plan(g, g->Lptr, g->nL, g->planL))) return rc;
         if ((rc = build_plan(g, g->Hptr, g->nH, g->planH))) return rc;
     }
+    g->heavy_plan = false;
+    if (heavy_pull_wanted() && !(DS_PULL_LIGHT || DS_PULL_HEAVY) && g->nH > 0) {
+        // standalone heavy pull for the giant heavy steps (needs A^T == A)
+        if (!g->sym_checked) {
+            if ((rc = check_symmetric(g))) return rc;
+            g->sym_checked = true;
+        }
+        if (g->symmetric) {
+            ds_graph::Plan& pl = g->planH;
+            if (!pl.rowid) {
+                CK(cudaMalloc(&pl.rowid, sizeof(int) * n));
+                CK(cudaMalloc(&pl.cptr, sizeof(long long) * (n + 1)));
+                CK(cudaMalloc(&pl.span, sizeof(int) * n));
+                CK(cudaMalloc(&pl.chunk_row, sizeof(unsigned) * (g->nnz / kChunk + 4)));
+            }
+            if (!g->req) CK(cudaMalloc(&g->req, sizeof(unsigned long long) * n));
+            if ((rc = build_plan(g, g->Hptr, g->nH, pl))) return rc;
+            g->heavy_plan = true;
+        }
+    }
     if (g->req && mode == DS_MODE_FIXED32)
         k_fill<unsigned><<<elementwise_grid(g), 256, 0, g->stream>>>((unsigned*)g->req, g->n, ModeFixed::INF);
     else if (g->req)
@@ -1324,6 +1359,9 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         // giant-push handoff off by default: since the push loop stopped
         // spilling, the in-kernel heavy push is faster than a standalone launch
         p.big_heavy = bh ? (unsigned long long)atoll(bh) : ~0ull;
+        // giant heavy steps (over half of A_H) as a standalone pull when A is symmetric
+        p.heavy_pull = g->heavy_plan ? 1 : 0;
+        if (g->heavy_plan && !bh) p.big_heavy = (unsigned long long)(g->nH / 2);
         if (grid < full_grid(g)) {
             // concurrent batch contexts: a full-device standalone push would
             // stall the other contexts' grids (measured slower), so no handoff
@@ -1394,10 +1432,15 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         const unsigned rgrid = (unsigned)(g->nsm * (h.rs_req == 1 ? g->occ_big_l : g->occ_big_h));
         ++x.launches;
         const int bsm = big_smem(sizeof(WarpSmem<typename M::D>));
-        if (h.rs_req == 1)
+        if (h.rs_req == 1) {
             k_big_relax<M, true><<<rgrid, kBigThreads, bsm, x.stream>>>(p);
-        else
+        } else if (h.rs_req == 3) {
+            ++x.launches;
+            k_big_pull<M><<<rgrid, kBigThreads, bsm, x.stream>>>(p);
+            k_big_commit<M><<<rgrid, kBigThreads, bsm, x.stream>>>(p);
+        } else {
             k_big_relax<M, false><<<rgrid, kBigThreads, bsm, x.stream>>>(p);
+        }
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(x.ev1, x.stream));

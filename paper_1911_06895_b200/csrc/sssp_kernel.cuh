@@ -241,6 +241,7 @@ struct KParams {
     int pull_enabled;
     float pull_light, pull_heavy;  // pull when push volume > frac * nnz
     unsigned long long big_light, big_heavy;  // pushes with >= this many edges run standalone
+    int heavy_pull;  // standalone heavy step as a pull (k_big_pull/k_big_commit; A^T == A)
     unsigned long long local_edges, local_entries;  // SMALL kernel: CTA-0-only steps below these
     long long ceiling;
     unsigned long long timeout_ns;
@@ -933,8 +934,8 @@ __device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot
     WarpSmem<D>& ws = sm.w[wib];
     unsigned qn = 0;
     const unsigned long long nchunk = ((unsigned long long)pl.nnz + kChunk - 1) / kChunk;
-    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
-    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * (blockDim.x >> 5);
     const unsigned long long pol = evict_first_policy();
     bool overflow = false;
     for (unsigned long long c = gw; c < nchunk; c += nw) {
@@ -968,8 +969,8 @@ __device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot
         const long long left = e1 - e0 - lane;
         Edge ed[kRelPer];
 #pragma unroll
-        for (int j = 0; j < kRelPer; ++j)
-            if (32 * j < left) ed[j] = M::load(edges + (e0 + lane + 32 * j), pol);
+        for (int j = 0; j < kRelPer; ++j)  // defined on every path (no loop-carried spill)
+            ed[j] = (32 * j < left) ? M::load(edges + (e0 + lane + 32 * j), pol) : Edge{};
         // Heavy gate reads go through L1: within a heavy pull the S bits and S
         // values are frozen, and L1 is invalidated at every grid barrier
         // (gpu-scope fence -> CCTL.IVALL).
@@ -978,6 +979,7 @@ __device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             gate[j] = false;
+            du[j] = (D)0;
             if (32 * j < left) {
                 const unsigned u = M::col(ed[j]);
                 if (LIGHT) {
@@ -985,7 +987,7 @@ __device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot
                     gate[j] = du[j] >= L && du[j] < H;
                 } else {
                     gate[j] = (p.sbits[u >> 5] >> (u & 31)) & 1u;
-                    if (gate[j]) du[j] = p.dist[u];
+                    du[j] = gate[j] ? p.dist[u] : (D)0;
                 }
             }
         }
@@ -1045,8 +1047,8 @@ __device__ void commit_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSl
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem<D>& ws = sm.w[wib];
     unsigned qn = 0;
-    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
-    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * (blockDim.x >> 5);
     for (unsigned long long b = gw * 32; b < (unsigned long long)pl.nspan; b += nw * 32) {
         const unsigned long long i = b + lane;
         bool want = false;
@@ -1413,7 +1415,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             }
             const unsigned long long E = heavy_done ? 0ull : (re & kMask33);
             if (E >= p.big_heavy) {
-                handoff(POS_AFTER_HEAVY, 2, E, re >> kPackShift);
+                handoff(POS_AFTER_HEAVY, p.heavy_pull ? 3 : 2, E, re >> kPackShift);
                 return;
             }
             if (DS_PULL_HEAVY && E > pullH) {
@@ -1529,6 +1531,37 @@ __global__ void __launch_bounds__(kBigThreads, DS_BIG_MINB) k_big_relax(const KP
         relax_step<M, true>(p, sm, &c->xslot, E, Rc, p.Ledges, H, p.F[pp], p.fbits[phases & 1]);
     else
         relax_step<M, false>(p, sm, &c->xslot, E, Rc, p.Hedges, H, nullptr, nullptr);
+    (void)L;
+}
+
+// The handed-off heavy step as the reference's own gathered form
+// (vxm_min_plus over A_H^T = A_H, gated by S membership; fused.py:105-124):
+// every row of A_H is streamed once (coalesced, evict-first) and the random
+// accesses are S-bit and S-value reads of hub ids, which stay in L1 -- versus
+// one random target check per pushed edge.  Rows crossing a chunk boundary
+// finish in k_big_commit.  Results land in Ctl::xslot like k_big_relax's.
+template <class M>
+__global__ void __launch_bounds__(kBigThreads, DS_BIG_MINB) k_big_pull(const KParams<M> p) {
+    using D = typename M::D;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
+    Ctl* const c = p.ctl;
+    const long long idx = ldcg(&c->rs_idx);
+    D L, H;
+    M::window((double)idx * p.delta, (double)(idx + 1) * p.delta, p.frac, L, H);
+    pull_step<M, false>(p, sm, &c->xslot, p.Hpull, p.Hedges, L, H, nullptr, nullptr);
+}
+
+template <class M>
+__global__ void __launch_bounds__(kBigThreads, DS_BIG_MINB) k_big_commit(const KParams<M> p) {
+    using D = typename M::D;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
+    Ctl* const c = p.ctl;
+    const long long idx = ldcg(&c->rs_idx);
+    D L, H;
+    M::window((double)idx * p.delta, (double)(idx + 1) * p.delta, p.frac, L, H);
+    commit_step<M, false>(p, sm, &c->xslot, p.Hpull, H, nullptr, nullptr);
     (void)L;
 }
 

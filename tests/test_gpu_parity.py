@@ -310,19 +310,23 @@ print("handoff ok")
 
 
 def test_giant_push_handoff_is_exact():
-    """Every push handed to the standalone k_big_relax launch (thresholds
-    forced down): the resumed persistent kernel stays bit-exact."""
+    """Every push handed to a standalone launch (thresholds forced down): the
+    light ones to k_big_relax, the heavy ones to the gathered heavy step
+    (k_big_pull + k_big_commit) on symmetric graphs or to k_big_relax
+    (DS_HEAVY_PULL=0, and always for the directed ER graph); the resumed
+    persistent kernel stays bit-exact."""
     import os
     import subprocess
     import sys
 
     from paper_1911_06895_b200.build import REPO
 
-    env = dict(os.environ, DS_BIG_L="64", DS_BIG_H="64", REPO=REPO)
-    r = subprocess.run([sys.executable, "-c", _HANDOFF_SCRIPT], env=env, capture_output=True,
-                       text=True, timeout=900)
-    assert r.returncode == 0, r.stdout + r.stderr
-    assert "handoff ok" in r.stdout
+    for pull in ("1", "0"):
+        env = dict(os.environ, DS_BIG_L="64", DS_BIG_H="64", DS_HEAVY_PULL=pull, REPO=REPO)
+        r = subprocess.run([sys.executable, "-c", _HANDOFF_SCRIPT], env=env, capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert "handoff ok" in r.stdout
 
 
 def test_block_local_kernel_is_exact():
