@@ -140,7 +140,10 @@ static_assert(kBigThreads % 32 == 0 && kBigThreads <= kThreads, "standalone push
 #endif
 constexpr int kChunk = DS_CHUNK;  // relax / pull: edges per warp chunk (32 lanes x kRelPer)
 constexpr int kRelPer = kChunk / 32;
-constexpr int kListPer = 4;       // capture (list): entries per lane
+#ifndef DS_LIST_PER
+#define DS_LIST_PER 2
+#endif
+constexpr int kListPer = DS_LIST_PER;  // capture (list): entries per lane
 constexpr int kRangePer = 16;     // capture (range): vertices per lane
 constexpr int kQueue = 256;       // per-warp append staging (overflow spills to global)
 #ifndef DS_HEAVY_RED
