@@ -1241,6 +1241,10 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
         per = q > 4e18 ? (LLONG_MAX / 4) : (long long)q + 2;
     }
     g->ceiling = per > LLONG_MAX / n ? LLONG_MAX : n * per;
+    // the push's shared-memory row bases are 32-bit edge indices
+    if (g->nL >= (1LL << 32) || g->nH >= (1LL << 32))
+        return set_err(DS_EINVAL, "light or heavy edge count %lld exceeds 2^32",
+                       std::max(g->nL, g->nH));
     const size_t esz = mode == DS_MODE_FIXED32 ? sizeof(uint2) : sizeof(EdgeF64);
     if ((rc = ensure_edges(&g->Ledges, &g->Lcap, esz * (size_t)g->nL))) return rc;
     if ((rc = ensure_edges(&g->Hedges, &g->Hcap, esz * (size_t)g->nH))) return rc;

@@ -144,8 +144,11 @@ constexpr int kRelPer = kChunk / 32;
 #define DS_LIST_PER 2
 #endif
 constexpr int kListPer = DS_LIST_PER;  // capture (list): entries per lane
+#ifndef DS_QUEUE
+#define DS_QUEUE 256
+#endif
 constexpr int kRangePer = 16;     // capture (range): vertices per lane
-constexpr int kQueue = 256;       // per-warp append staging (overflow spills to global)
+constexpr int kQueue = DS_QUEUE;  // per-warp append staging (overflow spills to global)
 #ifndef DS_HEAVY_RED
 #define DS_HEAVY_RED 0
 #endif
@@ -275,9 +278,10 @@ struct KParams {
 
 template <class D>
 struct WarpSmem {
-    long long base[kChunk + 1];
+    unsigned base[kChunk + 1];  // push: (row base + chunk offset) mod 2^32; pull: row end
+                                // (light / heavy edge arrays hold < 2^32 edges; checked at prepare)
     D d[kChunk + 1];
-    int rel[kChunk + 1];
+    short rel[kChunk + 1];  // chunk-relative row starts, clamped to [-1, kChunk]
     unsigned short row[kChunk];
     int q[kQueue];
 #if DS_PULL_LIGHT || DS_PULL_HEAVY
@@ -752,8 +756,8 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         for (int k = lane; k < ne; k += 32) {
             const unsigned long long r = r0 + k;
             const long long rel = ldcg(p.Rpre + r) - cb;
-            ws.rel[k] = rel < 0 ? 0 : (int)rel;
-            ws.base[k] = ldcg(p.Rbase + r);
+            ws.rel[k] = (short)(rel < 0 ? 0 : rel);
+            ws.base[k] = (unsigned)(ldcg(p.Rbase + r) + cb);
             ws.d[k] = __ldcg(p.Rd + r);
         }
         __syncwarp();
@@ -808,7 +812,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             const int kj = ws.row[r];
             // unconditional definition: a conditionally assigned ed[] is
             // loop-carried and was spilled to local memory
-            ed[j] = (32 * j < left) ? M::load(edges + (ws.base[kj] + cb + r), pol) : Edge{};
+            ed[j] = (32 * j < left) ? M::load(edges + (unsigned)(ws.base[kj] + r), pol) : Edge{};
             ws.du[r] = ws.d[kj];
         }
         __syncwarp();
@@ -822,7 +826,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             kk[j] = ws.row[r];
             // unconditional definition: a conditionally assigned ed[] is
             // loop-carried and was spilled to local memory
-            ed[j] = (32 * j < left) ? M::load(edges + (ws.base[kk[j]] + cb + r), pol) : Edge{};
+            ed[j] = (32 * j < left) ? M::load(edges + (unsigned)(ws.base[kk[j]] + r), pol) : Edge{};
         }
 #define DS_DU(j) ws.d[kk[j]]
 #endif
@@ -948,8 +952,9 @@ __device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot
         const int k1 = (int)__ldg(pl.chunk_row + c + 1);
         const int ne = k1 - k0 + 1;
         for (int i = lane; i < ne; i += 32) {
-            ws.rel[i] = (int)(__ldg(pl.cptr + k0 + i) - e0);   // may be < 0 (row began earlier)
-            ws.base[i] = __ldg(pl.cptr + k0 + i + 1);           // row end
+            const long long rs = __ldg(pl.cptr + k0 + i) - e0;  // < 0: row began earlier
+            ws.rel[i] = (short)(rs < 0 ? -1 : rs);
+            ws.base[i] = (unsigned)__ldg(pl.cptr + k0 + i + 1);  // row end
             ws.d[i] = M::INF;                                   // row minimum
         }
         __syncwarp();
@@ -1024,7 +1029,7 @@ __device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot
                 const D rmin = ws.d[i];
                 if (rmin != M::INF) {
                     rr = __ldg(pl.rowid + k0 + i);
-                    if (ws.rel[i] >= 0 && ws.base[i] <= e1) {
+                    if (ws.rel[i] >= 0 && (long long)ws.base[i] <= e1) {
                         pull_row_commit<M, LIGHT>(p, rmin, rr, H, want, val);
                     } else {
                         atomicMin(p.req + (k0 + i), rmin);  // row continues in other chunks

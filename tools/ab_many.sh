@@ -1,4 +1,4 @@
-# same-run A/B over several library builds / env settings (R-MAT 24 and 18)
+# same-run A/B over several library builds (R-MAT 24, R-MAT 18, grid 2048)
 L=paper_1911_06895_b200/lib
 run() { # name, lib, env...
   local n=$1 lib=$2; shift 2
@@ -8,3 +8,4 @@ run() { # name, lib, env...
 for r in 1 2; do
 for v in $@; do run $v $v; done
 done
+for v in $@; do DS_LIB=$L/libdsssp_$v.so python tools/trace_grid.py 2048 | head -1 | sed "s/^/$v /"; done
