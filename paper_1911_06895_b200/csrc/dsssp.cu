@@ -854,6 +854,23 @@ static int alloc_scratch(ds_graph* g) {
                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm6));
     CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeF64, true>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, sm6));
+    {   // smallest shared-memory carveout that fits one CTA: the rest of the
+        // 256 KB L1/shared array caches the pre-check distance reads
+        // (DS_CARVEOUT=<percent> overrides, -1 = driver default)
+        int pct_f = (int)std::min(100.0, std::ceil(100.0 * (smf + 1024) / (228.0 * 1024)));
+        int pct_6 = (int)std::min(100.0, std::ceil(100.0 * (sm6 + 1024) / (228.0 * 1024)));
+        if (const char* e = getenv("DS_CARVEOUT")) pct_f = pct_6 = atoi(e);
+        if (pct_f >= 0) {
+            CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeFixed, false>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, pct_f));
+            CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeFixed, true>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, pct_f));
+            CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeF64, false>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, pct_6));
+            CK(cudaFuncSetAttribute(sssp_persistent_kernel<ModeF64, true>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, pct_6));
+        }
+    }
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sssp_persistent_kernel<ModeFixed, false>,
                                                      kThreads, smf));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, sssp_persistent_kernel<ModeFixed, true>,
