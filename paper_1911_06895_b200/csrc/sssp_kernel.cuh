@@ -166,6 +166,9 @@ constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 #ifndef DS_PULL_HEAVY
 #define DS_PULL_HEAVY 0
 #endif
+#ifndef DS_ROWMAP_SCAN
+#define DS_ROWMAP_SCAN 1  // 1: push row map by marks + warp max-scan (0: search + walk)
+#endif
 #ifndef DS_DEFER_APPEND
 #define DS_DEFER_APPEND 1  // 1: consume a chunk's dedup claims after the next chunk's loads
 #endif
@@ -282,7 +285,7 @@ struct WarpSmem {
                                 // (light / heavy edge arrays hold < 2^32 edges; checked at prepare)
     D d[kChunk + 1];
     short rel[kChunk + 1];  // chunk-relative row starts, clamped to [-1, kChunk]
-    unsigned short row[kChunk];
+    alignas(16) unsigned short row[kChunk];
     int q[kQueue];
 #if DS_PULL_LIGHT || DS_PULL_HEAVY
     D qv[kQueue];  // values travelling with pull-produced lists
@@ -753,6 +756,44 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         const unsigned long long r1 = (c + 1 < nchunk) ? ldcg(p.chunk_start + c + 1) : Rc - 1;
         const int ne = (int)(r1 - r0 + 1);
         const long long cb = (long long)(c * kChunk);
+#if DS_ROWMAP_SCAN
+        // row map by marks + prefix max: entry k marks the chunk edge where
+        // its row starts, then every edge takes the largest mark at or
+        // before it (one warp scan instead of a per-lane search and walk)
+        static_assert(kRelPer == 8, "row-map scan assumes 8 edges per lane");
+        reinterpret_cast<uint4*>(ws.row)[lane] = make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+        for (int k = lane; k < ne; k += 32) {
+            const unsigned long long r = r0 + k;
+            const long long rel = ldcg(p.Rpre + r) - cb;
+            // the entry of chunk_start[c + 1] may begin exactly at the next chunk
+            if (rel < kChunk) ws.row[rel < 0 ? 0 : rel] = (unsigned short)k;
+            ws.base[k] = (unsigned)(ldcg(p.Rbase + r) + cb);
+            ws.d[k] = __ldcg(p.Rd + r);
+        }
+        __syncwarp();
+        {
+            uint4 m4 = reinterpret_cast<uint4*>(ws.row)[lane];
+            unsigned v[8] = {m4.x & 0xFFFFu, m4.x >> 16, m4.y & 0xFFFFu, m4.y >> 16,
+                             m4.z & 0xFFFFu, m4.z >> 16, m4.w & 0xFFFFu, m4.w >> 16};
+#pragma unroll
+            for (int j = 1; j < 8; ++j) v[j] = max(v[j], v[j - 1]);
+            unsigned run = v[7];  // inclusive max-scan of the lanes' maxima
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned t = __shfl_up_sync(0xffffffffu, run, o);
+                if (lane >= o) run = max(run, t);
+            }
+            unsigned carry = __shfl_up_sync(0xffffffffu, run, 1);
+            if (lane == 0) carry = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = max(v[j], carry);
+            m4 = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16),
+                            v[6] | (v[7] << 16));
+            reinterpret_cast<uint4*>(ws.row)[lane] = m4;
+        }
+        __syncwarp();
+#else
         for (int k = lane; k < ne; k += 32) {
             const unsigned long long r = r0 + k;
             const long long rel = ldcg(p.Rpre + r) - cb;
@@ -775,6 +816,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             ws.row[rel0 + j] = (unsigned short)k;
         }
         __syncwarp();
+#endif
     };
 #if DS_PIPE
     if (gw < nchunk) load_meta(gw);
