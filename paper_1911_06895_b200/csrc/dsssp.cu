@@ -11,6 +11,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include <algorithm>
@@ -1209,6 +1210,49 @@ static int split_counts(ds_graph* g, double delta, bool relabel, PrepStats* st) 
     return DS_OK;
 }
 
+__global__ void k_unpack_edges(const uint2* e, long long m, unsigned* key, unsigned* val) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+         i += (long long)gridDim.x * blockDim.x) {
+        const uint2 x = e[i];
+        key[i] = x.x;
+        val[i] = x.y;
+    }
+}
+__global__ void k_pack_edges(const unsigned* key, const unsigned* val, long long m, uint2* e) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
+         i += (long long)gridDim.x * blockDim.x)
+        e[i] = make_uint2(key[i], val[i]);
+}
+
+// Sort every row of a fixed-point edge array by (solver) target id: hubs,
+// which have the smallest ids, come first in every row, so the lanes of a
+// push chunk check neighbouring distance words (DS_SORT_ROWS=1).
+static int sort_rows(ds_graph* g, uint2* edges, const long long* ptr, long long m) {
+    if (m <= 1 || m > 0x7FFFFFFFLL) return DS_OK;
+    unsigned *k0 = nullptr, *k1 = nullptr, *v0 = nullptr, *v1 = nullptr;
+    int rc = DS_OK;
+    CK(cudaMalloc(&k0, sizeof(unsigned) * m));
+    CK(cudaMalloc(&k1, sizeof(unsigned) * m));
+    CK(cudaMalloc(&v0, sizeof(unsigned) * m));
+    CK(cudaMalloc(&v1, sizeof(unsigned) * m));
+    k_unpack_edges<<<elementwise_grid(g), 256, 0, g->stream>>>(edges, m, k0, v0);
+    CK(cudaGetLastError());
+    size_t bytes = 0;
+    CK(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, k0, k1, v0, v1, (int)m, (int)g->n, ptr,
+                                           ptr + 1, g->stream));
+    if ((rc = ensure_cub(g, bytes))) return rc;
+    CK(cub::DeviceSegmentedSort::SortPairs(g->cub_tmp, bytes, k0, k1, v0, v1, (int)m, (int)g->n, ptr,
+                                           ptr + 1, g->stream));
+    k_pack_edges<<<elementwise_grid(g), 256, 0, g->stream>>>(k1, v1, m, edges);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(g->stream));
+    cudaFree(k0);
+    cudaFree(k1);
+    cudaFree(v0);
+    cudaFree(v1);
+    return rc;
+}
+
 static int prepare(ds_graph* g, double delta, uint32_t flags) {
     if (!(delta > 0) || !std::isfinite(delta))
         return set_err(DS_EINVAL, "delta must be a positive finite number, got %g", delta);
@@ -1277,6 +1321,13 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
                                                               (EdgeF64*)g->Ledges,
                                                               (EdgeF64*)g->Hedges);
     CK(cudaGetLastError());
+    if (mode == DS_MODE_FIXED32) {
+        const char* e = getenv("DS_SORT_ROWS");
+        if (e && atoi(e)) {
+            if ((rc = sort_rows(g, (uint2*)g->Ledges, g->Lptr, g->nL))) return rc;
+            if ((rc = sort_rows(g, (uint2*)g->Hedges, g->Hptr, g->nH))) return rc;
+        }
+    }
     if (g->symmetric && (DS_PULL_LIGHT || DS_PULL_HEAVY)) {  // pull schedules (A^T == A)
         if ((rc = build_plan(g, g->Lptr, g->nL, g->planL))) return rc;
         if ((rc = build_plan(g, g->Hptr, g->nH, g->planH))) return rc;
