@@ -760,8 +760,11 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         // row map by marks + prefix max: entry k marks the chunk edge where
         // its row starts, then every edge takes the largest mark at or
         // before it (one warp scan instead of a per-lane search and walk)
-        static_assert(kRelPer == 8, "row-map scan assumes 8 edges per lane");
-        reinterpret_cast<uint4*>(ws.row)[lane] = make_uint4(0u, 0u, 0u, 0u);
+        static_assert(kRelPer == 8 || kRelPer == 4, "row-map scan: 4 or 8 edges per lane");
+        if (kRelPer == 8)
+            reinterpret_cast<uint4*>(ws.row)[lane] = make_uint4(0u, 0u, 0u, 0u);
+        else
+            reinterpret_cast<uint2*>(ws.row)[lane] = make_uint2(0u, 0u);
         __syncwarp();
         for (int k = lane; k < ne; k += 32) {
             const unsigned long long r = r0 + k;
@@ -773,12 +776,20 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         }
         __syncwarp();
         {
-            uint4 m4 = reinterpret_cast<uint4*>(ws.row)[lane];
-            unsigned v[8] = {m4.x & 0xFFFFu, m4.x >> 16, m4.y & 0xFFFFu, m4.y >> 16,
-                             m4.z & 0xFFFFu, m4.z >> 16, m4.w & 0xFFFFu, m4.w >> 16};
+            unsigned w[kRelPer / 2];  // the lane's kRelPer marks, two per word
+            if constexpr (kRelPer == 8) {
+                const uint4 m4 = reinterpret_cast<uint4*>(ws.row)[lane];
+                w[0] = m4.x; w[1] = m4.y; w[2] = m4.z; w[3] = m4.w;
+            } else {
+                const uint2 m2 = reinterpret_cast<uint2*>(ws.row)[lane];
+                w[0] = m2.x; w[1] = m2.y;
+            }
+            unsigned v[kRelPer];
 #pragma unroll
-            for (int j = 1; j < 8; ++j) v[j] = max(v[j], v[j - 1]);
-            unsigned run = v[7];  // inclusive max-scan of the lanes' maxima
+            for (int j = 0; j < kRelPer; ++j) v[j] = (j & 1) ? (w[j / 2] >> 16) : (w[j / 2] & 0xFFFFu);
+#pragma unroll
+            for (int j = 1; j < kRelPer; ++j) v[j] = max(v[j], v[j - 1]);
+            unsigned run = v[kRelPer - 1];  // inclusive max-scan of the lanes' maxima
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const unsigned t = __shfl_up_sync(0xffffffffu, run, o);
@@ -787,10 +798,13 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             unsigned carry = __shfl_up_sync(0xffffffffu, run, 1);
             if (lane == 0) carry = 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = max(v[j], carry);
-            m4 = make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16),
-                            v[6] | (v[7] << 16));
-            reinterpret_cast<uint4*>(ws.row)[lane] = m4;
+            for (int j = 0; j < kRelPer; ++j) v[j] = max(v[j], carry);
+#pragma unroll
+            for (int j = 0; j < kRelPer / 2; ++j) w[j] = v[2 * j] | (v[2 * j + 1] << 16);
+            if constexpr (kRelPer == 8)
+                reinterpret_cast<uint4*>(ws.row)[lane] = make_uint4(w[0], w[1], w[2], w[3]);
+            else
+                reinterpret_cast<uint2*>(ws.row)[lane] = make_uint2(w[0], w[1]);
         }
         __syncwarp();
 #else
