@@ -397,3 +397,44 @@ def test_batch_public_api_vs_oracle_and_overflow():
     assert delta_stepping_batch(a, [], 3.0) == []
     with pytest.raises(ValueError, match="out of range"):
         delta_stepping_batch(a, [0, 5000], 3.0)
+
+
+def test_reference_property_suites():
+    """The reference's own property tests for this path, on the GPU:
+    distances invariant across delta, skip mode never counts more outer
+    iterations (test_sssp.py:361-386), unit-weight connected graphs settle
+    bucket i at distance i (test_sssp.py:389-401)."""
+    from paper_1911_06895_b200 import random_connected_unit_graph, random_graph
+
+    deltas = (0.5, 1.0, 3.0, 11.0)
+    rng = np.random.default_rng(103)
+    for _ in range(15):
+        n = int(rng.integers(2, 50))
+        a = random_graph(n, int(rng.integers(1, 4 * n)), rng, weights="int")
+        source = int(rng.integers(0, n))
+        results = [delta_stepping(a, source, d) for d in deltas]
+        for r in results[1:]:
+            assert r.distances == results[0].distances
+        for d, r in zip(deltas, results):
+            sk = delta_stepping(a, source, d, skip_empty_buckets=True)
+            assert sk.distances == r.distances and sk.outer_iterations <= r.outer_iterations
+    rng = np.random.default_rng(107)
+    for _ in range(10):
+        n = int(rng.integers(2, 60))
+        a = random_connected_unit_graph(n, int(rng.integers(0, n)), rng)
+        r = delta_stepping(a, 0, 1.0)
+        want, _, _ = oracle.delta_stepping(a.n, a.indptr, a.col, a.val, 0, 1.0)
+        assert bits_equal(r.distances.to_dense(), want)
+        assert r.distances.nnz == n
+        assert r.outer_iterations == int(want.max()) + 1
+    # the same invariance at scale: R-MAT 16, four deltas, fixed-point mode
+    g = DeviceGraph.from_matrix(graphs.rmat(16, seed=5, weight_seed=6))
+    s = int(graphs.pick_sources(g.download()[0], 1, seed=1)[0])
+    base = None
+    for d in (0.05, 0.1, 0.25, 1.0):
+        st = g.solve(s, d)
+        assert st.dist_mode == 0
+        dd = g.result_dense()
+        base = dd if base is None else base
+        assert bits_equal(dd, base), d
+    g.close()
