@@ -438,3 +438,41 @@ def test_reference_property_suites():
         base = dd if base is None else base
         assert bits_equal(dd, base), d
     g.close()
+
+
+def test_device_resident_inputs_and_dtypes():
+    """ds_graph_create from device pointers (torch CUDA tensors) and from
+    pinned host tensors, with int32/int64 columns and f32/f64/i32 weights,
+    gives the host-numpy graph's results bit for bit."""
+    import torch
+
+    def T(x):  # the containers' arrays are read-only; torch wants writable memory
+        return torch.from_numpy(np.array(x))
+
+    a = graphs.rmat(14, seed=3, weight_seed=4)
+    s = int(graphs.pick_sources(a.indptr, 1, seed=2)[0])
+    want, outer, phases = oracle.delta_stepping(a.n, a.indptr, a.col, a.val, s, 0.1)
+    variants = [
+        (T(a.indptr).cuda(), T(a.col.astype(np.int32)).cuda(),
+         T(a.val.astype(np.float32)).cuda()),
+        (T(a.indptr).cuda(), T(a.col).cuda(),
+         T(a.val).cuda()),
+        (T(a.indptr).pin_memory(), T(a.col.astype(np.int32)).pin_memory(),
+         T(a.val.astype(np.float32)).pin_memory()),
+    ]
+    for ip, c, v in variants:
+        g = DeviceGraph.from_csr(a.n, ip, c, v)
+        st = g.solve(s, 0.1)
+        assert bits_equal(g.result_dense(), want)
+        assert (st.outer_iterations, st.inner_phases) == (outer, phases)
+        g.close()
+    # integer weights (i32) against the oracle
+    b = graphs.erdos_renyi(1024, seed=0)
+    g = DeviceGraph.from_csr(b.n, T(b.indptr).cuda(),
+                             T(b.col.astype(np.int32)).cuda(),
+                             T(b.val.astype(np.int32)).cuda())
+    st = g.solve(5, 3.0)
+    want, outer, phases = oracle.delta_stepping(b.n, b.indptr, b.col, b.val, 5, 3.0)
+    assert bits_equal(g.result_dense(), want)
+    assert (st.outer_iterations, st.inner_phases) == (outer, phases)
+    g.close()
