@@ -1089,9 +1089,16 @@ extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, co
         delete g;
         return rc;
     }
+    cudaStream_t vstream = nullptr;  // side stream of the weight upload
+    void* vstage = nullptr;
     auto fail = [&](int code) {
         std::string keep = g_err;
         cudaStreamSynchronize(g->stream);
+        if (vstream) {
+            cudaStreamSynchronize(vstream);
+            cudaStreamDestroy(vstream);
+        }
+        if (vstage) cudaFree(vstage);
         free_all(g);
         delete g;
         g_err = keep;
@@ -1140,27 +1147,28 @@ extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, co
             cudaFree(stage);
             stage = nullptr;
         }
-        // weights -> f64
+        // weights -> f64 on a side stream: their upload starts when the
+        // columns' has finished and overlaps the column check and the
+        // relabeling below (which only need indptr and col)
         const bool val_dev = is_device_ptr(val);
+        CKG(cudaEventRecord(g->ev0, g->stream));
+        CKG(cudaStreamCreateWithFlags(&vstream, cudaStreamNonBlocking));
+        CKG(cudaStreamWaitEvent(vstream, g->ev0, 0));
         if (val_dtype == DS_W_F64) {
             CKG(cudaMemcpyAsync(g->w, val, 8 * nnz,
-                                val_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, g->stream));
+                                val_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, vstream));
         } else {
             const void* vsrc = val;
             if (!val_dev) {
-                CKG(cudaMalloc(&stage, 4 * nnz));
-                CKG(cudaMemcpyAsync(stage, val, 4 * nnz, cudaMemcpyHostToDevice, g->stream));
-                vsrc = stage;
+                CKG(cudaMalloc(&vstage, 4 * nnz));
+                CKG(cudaMemcpyAsync(vstage, val, 4 * nnz, cudaMemcpyHostToDevice, vstream));
+                vsrc = vstage;
             }
             if (val_dtype == DS_W_F32)
-                k_convert_w<float><<<grid, 256, 0, g->stream>>>((const float*)vsrc, g->w, nnz);
+                k_convert_w<float><<<grid, 256, 0, vstream>>>((const float*)vsrc, g->w, nnz);
             else
-                k_convert_w<int><<<grid, 256, 0, g->stream>>>((const int*)vsrc, g->w, nnz);
+                k_convert_w<int><<<grid, 256, 0, vstream>>>((const int*)vsrc, g->w, nnz);
             CKG(cudaGetLastError());
-            if (stage) {
-                CKG(cudaStreamSynchronize(g->stream));
-                cudaFree(stage);
-            }
         }
     }
     int h = 0;
@@ -1168,6 +1176,13 @@ extern "C" int ds_graph_create(int64_t n, int64_t nnz, const int64_t* indptr, co
     CKG(cudaStreamSynchronize(g->stream));
     if (h & 2) return fail(set_err(DS_EINVAL, "column index out of range for dimension %lld", (long long)n));
     if ((rc = compute_order(g))) return fail(rc);
+    if (vstream) {  // the weights are in before anything reads them
+        CKG(cudaStreamSynchronize(vstream));
+        cudaStreamDestroy(vstream);
+        vstream = nullptr;
+        if (vstage) cudaFree(vstage);
+        vstage = nullptr;
+    }
     choose_kernel(g);
     if ((DS_PULL_LIGHT || DS_PULL_HEAVY) && (rc = check_symmetric(g))) return fail(rc);
 #undef CKG
