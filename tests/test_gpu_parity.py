@@ -476,3 +476,22 @@ def test_device_resident_inputs_and_dtypes():
     assert bits_equal(g.result_dense(), want)
     assert (st.outer_iterations, st.inner_phases) == (outer, phases)
     g.close()
+
+
+def test_batch_into_device_buffer():
+    """ds_sssp_batch writing its k x n results straight into device memory."""
+    import torch
+
+    a = graphs.rmat(15, seed=8, weight_seed=9)
+    g = DeviceGraph.from_matrix(a)
+    srcs = list(graphs.pick_sources(a.indptr, 5, seed=4))
+    out = torch.empty((len(srcs), a.n), dtype=torch.float64, device="cuda")
+    stats, none = g.solve_batch(srcs, 0.1, concurrency=2, out=int(out.data_ptr()))
+    assert none is None
+    torch.cuda.synchronize()
+    host = out.cpu().numpy()
+    for i, s in enumerate(srcs):
+        st = g.solve(s, 0.1)
+        assert bits_equal(host[i], g.result_dense())
+        assert stats[i].inner_phases == st.inner_phases
+    g.close()
