@@ -169,6 +169,9 @@ constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 #ifndef DS_ROWMAP_SCAN
 #define DS_ROWMAP_SCAN 1  // 1: push row map by marks + warp max-scan (0: search + walk)
 #endif
+#ifndef DS_CS_PREFETCH
+#define DS_CS_PREFETCH 1  // 1: prefetch the next chunk's chunk-map words
+#endif
 #ifndef DS_DEFER_APPEND
 #define DS_DEFER_APPEND 1  // 1: consume a chunk's dedup claims after the next chunk's loads
 #endif
@@ -751,9 +754,26 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     bool overflow = false;
     // entries of chunk c -> this warp's smem (offset, row base, captured d)
     // and the row map: lane resolves the entry of chunk edges [8 lane, 8 lane + 8)
+    // DS_CS_PREFETCH: the chunk map words of a warp's next chunk are loaded one
+    // iteration early (two registers), taking a round trip off the chain
+    unsigned cs0 = 0, cs1 = 0;
+    auto cs_fetch = [&](unsigned long long c) {
+        if (c < nchunk) {
+            cs0 = ldcg(p.chunk_start + c);
+            cs1 = (c + 1 < nchunk) ? ldcg(p.chunk_start + c + 1) : (unsigned)(Rc - 1);
+        }
+    };
+    if (DS_CS_PREFETCH) cs_fetch(gw);
     auto load_meta = [&](unsigned long long c) {
-        const unsigned long long r0 = ldcg(p.chunk_start + c);
-        const unsigned long long r1 = (c + 1 < nchunk) ? ldcg(p.chunk_start + c + 1) : Rc - 1;
+        unsigned long long r0, r1;
+        if (DS_CS_PREFETCH) {
+            r0 = cs0;
+            r1 = cs1;
+            cs_fetch(c + nw);
+        } else {
+            r0 = ldcg(p.chunk_start + c);
+            r1 = (c + 1 < nchunk) ? ldcg(p.chunk_start + c + 1) : Rc - 1;
+        }
         const int ne = (int)(r1 - r0 + 1);
         const long long cb = (long long)(c * kChunk);
 #if DS_ROWMAP_SCAN
