@@ -25,7 +25,9 @@ from .io import (  # noqa: F401
     ValidationError,
     load_edge_list,
     load_graph,
+    load_csr,
     load_matrix_market,
+    save_csr,
 )
 from .sssp import (  # noqa: F401
     BackendChoice,
@@ -64,5 +66,7 @@ __all__ = [
     "load_edge_list",
     "load_graph",
     "load_matrix_market",
+    "load_csr",
+    "save_csr",
     "__version__",
 ]

@@ -99,3 +99,49 @@ def test_large_generated_edge_list_roundtrip(tmp_path):
         for k in range(m.indptr[a], m.indptr[a + 1]):
             got[(a, int(m.col[k]))] = float(m.val[k])
     assert got == dense
+
+
+def test_binary_csr_cache_roundtrip(tmp_path):
+    from paper_1911_06895_b200 import graphs
+
+    rng = np.random.default_rng(5)
+    cases = [
+        graphs.erdos_renyi(256, seed=1),                        # int weights -> f32 storage
+        graphs.random_graph(300, 2000, rng, weights="float"),   # arbitrary f64 weights
+        graphs.rmat(10, seed=3),                                # fp32-lattice weights
+    ]
+    for k, m in enumerate(cases):
+        labels = dio.LabelMap([int(x) for x in rng.permutation(10 * m.n)[: m.n] + 1])
+        for lab in (None, labels):
+            p = str(tmp_path / f"g{k}.csr")
+            dio.save_csr(p, m, lab)
+            got, glab = dio.load_csr(p)
+            assert got == m
+            got.check_invariants()
+            want = lab.externals if lab is not None else list(range(1, m.n + 1))
+            assert glab.externals == want
+            spec = dio.GraphFile(path=p, format="csr")
+            assert dio.load_graph(spec)[0] == m
+
+
+def test_binary_csr_cache_rejects_bad_files(tmp_path):
+    from paper_1911_06895_b200 import graphs
+
+    m = graphs.erdos_renyi(64, seed=2)
+    p = tmp_path / "g.csr"
+    dio.save_csr(str(p), m)
+    raw = p.read_bytes()
+    bad = tmp_path / "bad.csr"
+    for blob, msg in ((b"not a cache at all" * 8, "not a binary CSR cache"),
+                      (raw[: len(raw) - 16], "truncated"),
+                      (raw[:8] + (0).to_bytes(8, "little") + raw[16:], "corrupt binary CSR header")):
+        bad.write_bytes(blob)
+        with pytest.raises(ValueError, match=msg):
+            dio.load_csr(str(bad))
+    # row offsets that do not end at nnz
+    head = 64
+    broken = bytearray(raw)
+    broken[head + 8 * m.n: head + 8 * (m.n + 1)] = (m.nnz + 1).to_bytes(8, "little")
+    bad.write_bytes(bytes(broken))
+    with pytest.raises(ValueError, match="corrupt row offsets"):
+        dio.load_csr(str(bad))
