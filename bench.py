@@ -5,7 +5,8 @@
 Workload (BASELINE.json configs[3], the single-GPU headline): R-MAT scale 24,
 edge factor 16, a,b,c,d = .57,.19,.19,.05, symmetrised + deduplicated,
 fp32-lattice weights, delta = 0.1, seeded random sources with nonzero degree.
-One step = one batch of `--batch` sources solved on the resident graph through
+One step = the BASELINE workload: the whole 64-source pool (`--batch`, default
+64) solved on the resident graph through
 ds_sssp_batch, `--concurrency` sources in flight on SM-disjoint persistent
 grids (each source's result is exactly its single-source result).
 
@@ -55,7 +56,8 @@ def parse():
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edge-factor", type=int, default=16)
     ap.add_argument("--delta", type=float, default=0.1)
-    ap.add_argument("--batch", type=int, default=8, help="sources per step (per rank)")
+    ap.add_argument("--batch", type=int, default=64,
+                    help="sources per step (per rank); default = the BASELINE's 64-source pool")
     ap.add_argument("--sources", type=int, default=64, help="source pool (BASELINE: 64)")
     ap.add_argument("--concurrency", type=int, default=2,
                     help="sources in flight per GPU (ds_sssp_batch contexts; 1 = one at a time)")
