@@ -177,6 +177,7 @@ struct SolveCtx {
     long long *Rpre = nullptr, *Rbase = nullptr;
     void* Rd = nullptr;
     unsigned* chunk_start = nullptr;
+    void* csum = nullptr;  // scan-chunk bounds (SMALL kernel)
     Ctl* ctl = nullptr;
     Ctl* h_ctl = nullptr;
     double* out = nullptr;
@@ -242,6 +243,7 @@ struct ds_graph {
     long long* Rbase = nullptr;
     void* Rd = nullptr;
     unsigned* chunk_start = nullptr;
+    void* csum = nullptr;  // scan-chunk bounds (SMALL kernel)
     int* order = nullptr;  // solver id -> input id
     int* perm = nullptr;   // input id -> solver id
     long long n_active = 0;
@@ -291,6 +293,7 @@ static SolveCtx main_ctx(ds_graph* g) {
     x.Rbase = g->Rbase;
     x.Rd = g->Rd;
     x.chunk_start = g->chunk_start;
+    x.csum = g->csum;
     x.ctl = g->ctl;
     x.h_ctl = g->h_ctl;
     x.out = g->out;
@@ -310,12 +313,12 @@ static void free_all(ds_graph* g) {
                     g->planL.rowid, g->planL.cptr, g->planL.chunk_row, g->planL.span,
                     g->planH.rowid, g->planH.cptr, g->planH.chunk_row, g->planH.span,
                     g->Rbase,  g->Rd,   g->chunk_start, g->order, g->perm, g->ctl,
-                    g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace};
+                    g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace, g->csum};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (SolveCtx* x : g->extra) {
         void* q[] = {x->dist, x->fbits, x->sbits, x->F0, x->F1, x->S0, x->S1, x->Fv0, x->Fv1,
-                     x->req, x->Rpre, x->Rbase, x->Rd, x->chunk_start, x->ctl, x->out, x->out2};
+                     x->req, x->Rpre, x->Rbase, x->Rd, x->chunk_start, x->ctl, x->out, x->out2, x->csum};
         for (void* p : q)
             if (p) cudaFree(p);
         for (cudaEvent_t e : x->copied)
@@ -834,6 +837,7 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaMalloc(&g->Rbase, sizeof(long long) * n));
     CK(cudaMalloc(&g->Rd, sizeof(unsigned long long) * n));
     CK(cudaMalloc(&g->chunk_start, sizeof(unsigned) * (g->nnz / kChunk + 4)));
+    CK(cudaMalloc(&g->csum, sizeof(unsigned long long) * (n / (32 * kRangePer) + 2)));
     CK(cudaMalloc(&g->ctl, sizeof(Ctl)));
     g->h_ctl = new Ctl();
     CK(cudaMalloc(&g->pstat, sizeof(PrepStats)));
@@ -1451,6 +1455,11 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         // giant heavy steps (over half of A_H) as a standalone pull when A is symmetric
         p.heavy_pull = g->heavy_plan ? 1 : 0;
         if (g->heavy_plan && !bh) p.big_heavy = (unsigned long long)(g->nH / 2);
+        if (g->small && kCsum) {
+            // the standalone pushes do not maintain the SMALL kernel's scan-chunk
+            // bounds; SMALL graphs have tiny frontiers anyway
+            p.big_light = p.big_heavy = ~0ull;
+        }
         if (grid < full_grid(g)) {
             // concurrent batch contexts: a full-device standalone push would
             // stall the other contexts' grids (measured slower), so no handoff
@@ -1465,6 +1474,7 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     p.Rbase = x.Rbase;
     p.Rd = (typename M::D*)x.Rd;
     p.chunk_start = x.chunk_start;
+    p.csum = (typename M::D*)x.csum;
     p.perm = g->perm;
     p.n_active = g->n_active;
     p.ctl = x.ctl;
@@ -1648,6 +1658,7 @@ static int make_ctx(ds_graph* g, SolveCtx** out) {
     CK(cudaMalloc(&x->Rbase, sizeof(long long) * n));
     CK(cudaMalloc(&x->Rd, sizeof(unsigned long long) * n));
     CK(cudaMalloc(&x->chunk_start, sizeof(unsigned) * (g->nnz / kChunk + 4)));
+    CK(cudaMalloc(&x->csum, sizeof(unsigned long long) * (n / (32 * kRangePer) + 2)));
     CK(cudaMalloc(&x->ctl, sizeof(Ctl)));
     x->h_ctl = new Ctl();
     CK(cudaMalloc(&x->out, sizeof(double) * n));

@@ -166,6 +166,18 @@ constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 #ifndef DS_PULL_HEAVY
 #define DS_PULL_HEAVY 0
 #endif
+// DS_CSUM: the high-diameter (SMALL) kernel keeps, per 512-vertex scan chunk,
+// a lower bound of the stored values beyond the current window, so a bucket
+// scan reads only the chunks that can hold in-window vertices (the dense scan
+// of every vertex per bucket dominated many-bucket graphs).  Push builds only:
+// the pull forms write beyond-window values without maintaining the bound.
+#ifndef DS_CSUM
+#define DS_CSUM 1
+#endif
+#ifndef DS_CSUM_RED
+#define DS_CSUM_RED 1
+#endif
+constexpr bool kCsum = DS_CSUM && !(DS_PULL_LIGHT || DS_PULL_HEAVY);
 #ifndef DS_ROWMAP_SCAN
 #define DS_ROWMAP_SCAN 1  // 1: push row map by marks + warp max-scan (0: search + walk)
 #endif
@@ -264,6 +276,7 @@ struct KParams {
     const Edge* Hedges;
     PullPlan Lpull, Hpull;
     D* dist;
+    D* csum;             // SMALL kernel (kCsum): per scan chunk, <= every stored value >= the window
     D* req;              // pull partial minima (INF when idle), n_nz entries
     unsigned* fbits[2];  // next-frontier dedup bitmaps (alternating phases)
     unsigned* sbits;     // S membership / dedup bitmap
@@ -582,7 +595,7 @@ __device__ __forceinline__ void load_run<unsigned long long>(const unsigned long
 // RANGE capture: bucket extraction by a dense scan of the distance array.
 // Also retires the previous bucket's S bits (atomicAnd: disjoint from the
 // new bucket's S, which only holds vertices with values >= the old hi).
-template <class M>
+template <class M, bool SUM = false>
 __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                               typename M::D L, typename M::D H, int* S, unsigned long long* s_counter,
                               unsigned long long n_scan, const int* old_S, unsigned long long old_count) {
@@ -600,7 +613,7 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
     const unsigned long long per_chunk = 32ull * kRangePer;
     const unsigned long long nchunk = (n + per_chunk - 1) / per_chunk;
     unsigned long long local_fc = 0, local_min = ~0ull;
-    for (unsigned long long c = gw; c < nchunk; c += nw) {
+    auto scan_chunk = [&](unsigned long long c) {
         const unsigned long long v0 = c * per_chunk + (unsigned long long)lane * kRangePer;
         D dv[kRangePer];
         if (v0 + kRangePer <= n) {
@@ -610,13 +623,19 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
             for (int j = 0; j < kRangePer; ++j) dv[j] = v0 + j < n ? __ldcg(p.dist + v0 + j) : M::INF;
         }
         unsigned hits = 0;
+        unsigned long long cmin = ~0ull;
 #pragma unroll
         for (int j = 0; j < kRangePer; ++j) {
             const D d = dv[j];
-            if (d >= H && d != M::INF && (unsigned long long)d < local_min) local_min = (unsigned long long)d;
+            if (d >= H && d != M::INF && (unsigned long long)d < cmin) cmin = (unsigned long long)d;
             if (d >= L && d < H) hits |= 1u << j;
         }
-        if (!__any_sync(0xffffffffu, hits != 0)) continue;
+        if (cmin < local_min) local_min = cmin;
+        if (SUM) {  // exact bound for the chunk (no relaxation runs during this step)
+            cmin = warp_min(cmin);
+            if (lane == 0) p.csum[c] = cmin == ~0ull ? M::INF : (D)cmin;
+        }
+        if (!__any_sync(0xffffffffu, hits != 0)) return;
         local_fc += __popc(hits);
         // in-window vertices of this chunk, kListPer per lane per round
         D cd[kListPer];
@@ -658,6 +677,29 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
         }
         if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
             wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
+    };
+    if (SUM) {
+        // the warp's chunks are the usual grid-strided ones; each lane reads the
+        // bound of one of them (one round trip for up to 32 chunks) and the
+        // warp scans only the chunks whose bound is below hi.  Every stored value >= lo of a chunk is >= its
+        // bound, so a bound >= hi means no in-window vertex, and it stands in
+        // for the chunk's beyond-window minimum (a lower bound of it: a low
+        // bound only makes the solver visit an empty bucket, which is not
+        // counted and rescans that chunk exactly)
+        for (unsigned long long g = gw; g < nchunk; g += 32 * nw) {
+            const unsigned long long cl = g + lane * nw;
+            const D s = cl < nchunk ? __ldcg(p.csum + cl) : M::INF;
+            const bool act = s < H;
+            if (!act && s != M::INF && (unsigned long long)s < local_min) local_min = (unsigned long long)s;
+            unsigned mask = __ballot_sync(0xffffffffu, act);
+            while (mask) {
+                const int b = __ffs(mask) - 1;
+                mask &= mask - 1;
+                scan_chunk(g + (unsigned long long)b * nw);
+            }
+        }
+    } else {
+        for (unsigned long long c = gw; c < nchunk; c += nw) scan_chunk(c);
     }
     wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
     const unsigned long long fc = block_reduce<0>(local_fc, sm.red);
@@ -735,7 +777,19 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
 #endif
 // Inlined: a __noinline__ push measured 25% slower (the kernel parameters
 // then live in a local-memory frame).
-template <class M, bool LIGHT, bool LOCALW = false>
+template <class M>
+__device__ __forceinline__ void csum_lower(const KParams<M>& p, unsigned v, typename M::D nd) {
+    typename M::D* b = p.csum + v / (32u * kRangePer);
+#if DS_CSUM_RED
+    atomicMin(b, nd);  // result unused: a fire-and-forget reduction, no round trip
+#else
+    if (nd < *b) atomicMin(b, nd);  // a stale (L1) bound is >= the current one
+#endif
+}
+
+// SUM: also lower the scan-chunk bound of every target that may have received
+// a value beyond the window (SMALL kernel, see capture_range).
+template <class M, bool LIGHT, bool LOCALW = false, bool SUM = false>
 __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                            unsigned long long E, unsigned long long Rc,
                            const typename M::Edge* edges, typename M::D H, int* out_list,
@@ -939,6 +993,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             for (int j = 0; j < kRelPer; ++j) {
                 const unsigned v = M::col(ed[j]);
                 const bool want = 32 * j < left && nd[j] < old[j] && nd[j] < H;
+                if (SUM && 32 * j < left && nd[j] < old[j] && nd[j] >= H) csum_lower(p, v, nd[j]);
                 p_col[j] = v;
                 p_ret[j] = want ? atomicOr(fbits + (v >> 5), 1u << (v & 31)) : 0u;
                 p_req |= (want ? 1u : 0u) << j;
@@ -953,6 +1008,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                     got[j] = atomicOr(fbits + (v >> 5), 1u << (v & 31)) & (1u << (v & 31));
                     got[j] = got[j] ? 0u : 1u;
                 }
+                if (SUM && 32 * j < left && nd[j] < old[j] && nd[j] >= H) csum_lower(p, M::col(ed[j]), nd[j]);
             }
 #pragma unroll
             for (int j = 0; j < kRelPer; ++j)
@@ -964,7 +1020,10 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         } else {
 #pragma unroll
             for (int j = 0; j < kRelPer; ++j)
-                if (32 * j < left && nd[j] < cur[j]) atomicMin(p.dist + M::col(ed[j]), nd[j]);
+                if (32 * j < left && nd[j] < cur[j]) {
+                    atomicMin(p.dist + M::col(ed[j]), nd[j]);
+                    if (SUM) csum_lower(p, M::col(ed[j]), nd[j]);  // heavy values are >= hi
+                }
         }
         __syncwarp();
 #undef DS_DU
@@ -1167,6 +1226,7 @@ template <class M, bool SMALL>
 __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     sssp_persistent_kernel(const KParams<M> p) {
     using D = typename M::D;
+    constexpr bool kSum = SMALL && kCsum;  // scan-chunk bounds (high-diameter kernel only)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<D>& sm = *reinterpret_cast<Smem<D>*>(smem_raw);
     Ctl* const c = p.ctl;
@@ -1192,6 +1252,12 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         const long long stride = (long long)gridDim.x * kThreads;
         for (long long v = (long long)blockIdx.x * kThreads + threadIdx.x; v < n_scan; v += stride)
             p.dist[v] = (v == src) ? (D)0 : M::INF;
+        if (kSum) {
+            const long long per = 32ll * kRangePer;
+            for (long long k = (long long)blockIdx.x * kThreads + threadIdx.x; k < (n_scan + per - 1) / per;
+                 k += stride)
+                p.csum[k] = (k == src / per) ? (D)0 : M::INF;
+        }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             for (int k = 0; k < 3; ++k) {
                 StepSlot* s = &c->slot[k];
@@ -1290,7 +1356,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         if (pos == POS_BUCKET) {
             // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
             if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[bpar ^ 1] = 0;
-            capture_range<M>(p, sm, &c->slot[st % 3], L, H, p.S[bpar], &c->s_count[bpar],
+            capture_range<M, kSum>(p, sm, &c->slot[st % 3], L, H, p.S[bpar], &c->s_count[bpar],
                              (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount);
             old_scount = 0;
             if (!end_step(0, (unsigned long long)n_scan)) return;
@@ -1337,7 +1403,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                         const unsigned long long lE = lre & kMask33;
                         lesc += lE;
                         if (lE)
-                            relax_step<M, true, true>(p, sm, a, lE, lre >> kPackShift, p.Ledges, H,
+                            relax_step<M, true, true, kSum>(p, sm, a, lE, lre >> kPackShift, p.Ledges, H,
                                                       p.F[lpp], p.fbits[lph & 1]);
                         __syncthreads();
                         if (ldcg(&a->flags) & 1u) {
@@ -1419,7 +1485,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 continue;
             } else if (E > 0) {
                 escanned += E;
-                relax_step<M, true>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Ledges, H,
+                relax_step<M, true, false, kSum>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Ledges, H,
                                     p.F[pp], p.fbits[phases & 1]);
                 if (!end_step(1, E)) return;
                 if (ldcg(&prev()->flags) & 1u) {
@@ -1475,7 +1541,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                     if ((lre & kMask33) <= p.local_edges) {
                         escanned += lre & kMask33;
                         if (lre & kMask33)
-                            relax_step<M, false, true>(p, sm, a, lre & kMask33, lre >> kPackShift,
+                            relax_step<M, false, true, kSum>(p, sm, a, lre & kMask33, lre >> kPackShift,
                                                        p.Hedges, H, nullptr, nullptr);
                         __syncthreads();
                         done = 1;
@@ -1517,7 +1583,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 }
             } else if (E > 0) {
                 escanned += E;
-                relax_step<M, false>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Hedges, H,
+                relax_step<M, false, false, kSum>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Hedges, H,
                                      nullptr, nullptr);
                 if (!end_step(4, E)) return;
                 if (ldcg(&prev()->flags) & 1u) {
