@@ -110,7 +110,8 @@ int ds_sssp(ds_graph* g, int64_t source, double delta, uint32_t flags, ds_stats*
 /* k sources against one prepared graph (the reference's callers loop over
  * sources: cli.py:119-128, the 64/16-source benchmarks).  Up to `concurrency`
  * sources run at once on SM-disjoint persistent grids, each on its own
- * stream (0 = library default, DS_BATCH_CONC or 2).  stats: k entries or
+ * stream (0 = library default: DS_BATCH_CONC if set, else 8 for graphs below
+ * 24 Mi edges or high-diameter graphs, 2 otherwise).  stats: k entries or
  * NULL.  dist_out: k x n float64 (row i = dense distances of sources[i],
  * +inf = unreachable), host or device, or NULL to keep nothing.  A source
  * whose fixed-point solve overflows is rerun in binary64 (stats.fallbacks=1).

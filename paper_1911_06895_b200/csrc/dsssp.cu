@@ -1688,7 +1688,12 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
     // concurrency: solver contexts on SM-disjoint grids (0 = library default)
     int T = concurrency;
     if (T <= 0) {
-        T = 2;
+        // measured (tools/batch_probe.py, 16 sources): small and high-diameter
+        // graphs leave a full grid latency-bound, so 8 solves in flight pay
+        // (R-MAT 18 7.0 -> 18.1 GTEPS, R-MAT 19 13.0 -> 29.4, grid 2048^2
+        // 197 -> 50 ms/source); from R-MAT 20 (30 M edges) on, two do
+        // (R-MAT 20 23.1 -> 39.4, R-MAT 24 76.8 -> 83.5; 8 would cost 10-48%)
+        T = (g->small || g->nnz < (24LL << 20)) ? 8 : 2;
         if (const char* e = getenv("DS_BATCH_CONC")) T = std::max(1, atoi(e));
     }
     T = (int)std::min<long long>({(long long)T, (long long)k, 8LL, (long long)g->nsm});
