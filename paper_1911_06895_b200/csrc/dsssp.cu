@@ -1470,8 +1470,7 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         p.local_edges = le ? (unsigned long long)atoll(le) : 16384ull;
         p.local_entries = ln ? (unsigned long long)atoll(ln) : 4096ull;
     }
-    p.Rpre = x.Rpre;
-    p.Rbase = x.Rbase;
+    p.Rent = reinterpret_cast<uint2*>(x.Rpre);  // n entries of 8 B
     p.Rd = (typename M::D*)x.Rd;
     p.chunk_start = x.chunk_start;
     p.csum = (typename M::D*)x.csum;

@@ -505,8 +505,7 @@ static int shard_push(ds_shard* s, bool light, const int* ids, const unsigned lo
                       long long count, typename M::D H, long long* nf, int* ovf) {
     KParams<M> p{};
     p.dist = (typename M::D*)s->dist;
-    p.Rpre = s->Rpre;
-    p.Rbase = s->Rbase;
+    p.Rent = reinterpret_cast<uint2*>(s->Rpre);  // n entries of 8 B
     p.Rd = (typename M::D*)s->Rd;
     p.chunk_start = s->chunk_start;
     SCK(cudaMemsetAsync(s->slot, 0, sizeof(StepSlot), s->stream));

@@ -283,8 +283,8 @@ struct KParams {
     int* F[2];           // frontier lists
     D* Fv[2];            // frontier values (lists produced by a pull)
     int* S[2];           // S lists (alternating buckets)
-    long long* Rpre;
-    long long* Rbase;
+    uint2* Rent;  // capture entries {edge prefix, row base - prefix}, both mod 2^32
+                  // (a step's edges and the split arrays stay below 2^32, checked at prepare)
     D* Rd;
     unsigned* chunk_start;
     const int* perm;      // input id -> solver id (degree-sorted relabeling)
@@ -556,8 +556,7 @@ __device__ __forceinline__ void capture_emit(const KParams<M>& p, StepSlot* slot
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         if (deg[j] > 0) {
-            p.Rpre[rank] = (long long)pre;
-            p.Rbase[rank] = off[j] - (long long)pre;
+            p.Rent[rank] = make_uint2((unsigned)pre, (unsigned)(off[j] - (long long)pre));
             p.Rd[rank] = dv[j];
             const unsigned long long t0 = (pre + kChunk - 1) / kChunk;
             const unsigned long long t1 = (pre + (unsigned long long)deg[j] - 1) / kChunk;
@@ -842,10 +841,11 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         __syncwarp();
         for (int k = lane; k < ne; k += 32) {
             const unsigned long long r = r0 + k;
-            const long long rel = ldcg(p.Rpre + r) - cb;
+            const uint2 en = __ldcg(p.Rent + r);
+            const long long rel = (long long)en.x - cb;
             // the entry of chunk_start[c + 1] may begin exactly at the next chunk
             if (rel < kChunk) ws.row[rel < 0 ? 0 : rel] = (unsigned short)k;
-            ws.base[k] = (unsigned)(ldcg(p.Rbase + r) + cb);
+            ws.base[k] = en.y + (unsigned)cb;
             ws.d[k] = __ldcg(p.Rd + r);
         }
         __syncwarp();
@@ -884,9 +884,10 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
 #else
         for (int k = lane; k < ne; k += 32) {
             const unsigned long long r = r0 + k;
-            const long long rel = ldcg(p.Rpre + r) - cb;
+            const uint2 en = __ldcg(p.Rent + r);
+            const long long rel = (long long)en.x - cb;
             ws.rel[k] = (short)(rel < 0 ? 0 : rel);
-            ws.base[k] = (unsigned)(ldcg(p.Rbase + r) + cb);
+            ws.base[k] = en.y + (unsigned)cb;
             ws.d[k] = __ldcg(p.Rd + r);
         }
         __syncwarp();
