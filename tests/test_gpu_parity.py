@@ -495,3 +495,42 @@ def test_batch_into_device_buffer():
         assert bits_equal(host[i], g.result_dense())
         assert stats[i].inner_phases == st.inner_phases
     g.close()
+
+
+def _fixpoint_certificate(indptr, col, val, d_h, s):
+    """Size-independent exactness check (tools/rmat27_cert.py): over every
+    kept edge (w > 0, sssp.py:106-150) with finite d[u], min_u fl(d[u] + w)
+    is >= d[v] everywhere and == d[v] for every reached v != s."""
+    import torch
+
+    dev = torch.device("cuda:0")
+    n = len(indptr) - 1
+    d = torch.from_numpy(d_h).to(dev)
+    ip = torch.from_numpy(indptr).to(dev)
+    rows = torch.repeat_interleave(torch.arange(n, device=dev), ip[1:] - ip[:-1])
+    c = torch.from_numpy(col).to(dev).long()
+    w = torch.from_numpy(val).to(dev).double()
+    du = d[rows]
+    keep = (w > 0) & torch.isfinite(du)
+    best = torch.full((n,), float("inf"), dtype=torch.float64, device=dev)
+    best.scatter_reduce_(0, c[keep], (du + w)[keep], reduce="amin")
+    reached = torch.isfinite(d)
+    others = reached.clone()
+    others[s] = False
+    assert d_h[s] == 0.0
+    assert bool((best >= d).all()), "an edge still improves a distance"
+    assert bool((best[others] == d[others]).all()), "a distance is not achieved by any edge"
+    assert bool(torch.isinf(best[~reached]).all())
+
+
+@pytest.mark.parametrize("delta", [0.05, 0.25])
+def test_rmat22_fixpoint_certificate(delta):
+    g = DeviceGraph.rmat(22, 16, 1, 2)
+    try:
+        indptr, col, val = g.download()
+        g.prepare(delta)
+        for s in graphs.pick_sources(indptr, 2, seed=5):
+            g.solve(int(s), delta)
+            _fixpoint_certificate(indptr, col, val, g.result_dense(), int(s))
+    finally:
+        g.close()
