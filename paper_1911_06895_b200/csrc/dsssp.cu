@@ -162,6 +162,7 @@ struct PrepStats {
     int max_frac;
     int pad;
     unsigned long long nL, nH;
+    unsigned long long min_heavy_bits;
 };
 
 // Per-solve scratch and control.  The handle's own buffers form context 0
@@ -208,6 +209,7 @@ struct ds_graph {
     int frac = 0;
     long long nL = 0, nH = 0;
     double minL = INFINITY;
+    double minH = INFINITY;  // smallest heavy weight (heavy-pull landing check)
     long long ceiling = 0;
     double prep_ms = 0;
     double overflow_delta = NAN;  // delta whose fixed-point solve overflowed
@@ -444,7 +446,7 @@ __global__ void k_split_count(long long nnz, long long n, const long long* indpt
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     const long long per = ((nnz + nwarps - 1) / nwarps + 31) & ~31LL;
     const long long e_begin = warp * per, e_end = min(nnz, e_begin + per);
-    unsigned long long minL = ~0ull, maxw = 0, nl = 0, nh = 0;
+    unsigned long long minL = ~0ull, minH = ~0ull, maxw = 0, nl = 0, nh = 0;
     int frac = 0;
     if (e_begin < e_end) {
         long long r = warp_first_row(indptr, n, e_begin);
@@ -460,6 +462,7 @@ __global__ void k_split_count(long long nnz, long long n, const long long* indpt
                 if (L || H) {
                     const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
                     if (L && bits < minL) minL = bits;
+                    if (H && bits < minH) minH = bits;
                     if (bits > maxw) maxw = bits;
                     frac = max(frac, frac_bits(x));
                 }
@@ -478,11 +481,13 @@ __global__ void k_split_count(long long nnz, long long n, const long long* indpt
         }
     }
     minL = warp_min(minL);
+    minH = warp_min(minH);
     maxw = warp_max(maxw);
 #pragma unroll
     for (int o = 16; o; o >>= 1) frac = max(frac, __shfl_xor_sync(0xffffffffu, frac, o));
     if (lane == 0) {
         if (minL != ~0ull) atomicMin(&st->min_light_bits, minL);
+        if (minH != ~0ull) atomicMin(&st->min_heavy_bits, minH);
         if (maxw) atomicMax(&st->max_w_bits, maxw);
         if (frac) atomicMax(&st->max_frac, frac);
         if (nl) atomicAdd(&st->nL, nl);
@@ -1282,6 +1287,7 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     const long long n = g->n;
     PrepStats init{};
     init.min_light_bits = ~0ull;
+    init.min_heavy_bits = ~0ull;
     *g->h_pstat = init;
     CK(cudaEventRecord(g->ev0, g->stream));
     CK(cudaMemcpyAsync(g->pstat, g->h_pstat, sizeof(PrepStats), cudaMemcpyHostToDevice, g->stream));
@@ -1305,6 +1311,8 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     double maxw = 0;
     memcpy(&maxw, &st.max_w_bits, 8);
     g->minL = minL;
+    g->minH = INFINITY;
+    if (st.min_heavy_bits != ~0ull) memcpy(&g->minH, &st.min_heavy_bits, 8);
     // fixed point iff every weight is an integer multiple of 2^-frac and the
     // largest weight fits well inside 32 bits (runtime overflow is detected)
     int mode = DS_MODE_F64;
@@ -1350,6 +1358,12 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     if (g->symmetric && (DS_PULL_LIGHT || DS_PULL_HEAVY)) {  // pull schedules (A^T == A)
         if ((rc = build_plan(g, g->Lptr, g->nL, g->planL))) return rc;
         if ((rc = build_plan(g, g->Hptr, g->nH, g->planH))) return rc;
+    }
+    // direction-optimised heavy steps gather through A_H^T = A_H: symmetric
+    // graphs only (fingerprint computed once per graph)
+    if (!g->sym_checked && g->nH > 0) {
+        if ((rc = check_symmetric(g))) return rc;
+        g->sym_checked = true;
     }
     g->heavy_plan = false;
     if (heavy_pull_wanted() && !(DS_PULL_LIGHT || DS_PULL_HEAVY) && g->nH > 0) {
@@ -1464,6 +1478,21 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
             // concurrent batch contexts: a full-device standalone push would
             // stall the other contexts' grids (measured slower), so no handoff
             p.big_light = p.big_heavy = ~0ull;
+        }
+        // direction-optimised heavy step (see POS_HEAVY in sssp_kernel.cuh)
+        const char* hp = getenv("DS_HPULL");
+        p.hpull = (g->sym_checked && g->symmetric && g->nH > 0 && !(hp && atoi(hp) == 0)) ? 1 : 0;
+        const char* hr = getenv("DS_HPULL_RATIO");
+        p.hpull_ratio = hr ? (float)atof(hr) : 1.0f;
+        const char* hm = getenv("DS_HPULL_MIN");
+        p.hpull_min = hm ? (unsigned long long)atoll(hm) : (1ull << 20);
+        p.nH = (unsigned long long)g->nH;
+        if (g->mode == DS_MODE_FIXED32) {
+            const double W = std::isfinite(g->minH) ? ldexp(g->minH, g->frac) : 0.0;
+            p.min_heavy = (unsigned long long)W;  // exact: every weight is k * 2^-frac
+        } else {
+            double mh = std::isfinite(g->minH) ? g->minH : 0.0;
+            memcpy(&p.min_heavy, &mh, 8);
         }
         const char* le = getenv("DS_LOCAL_E");
         const char* ln = getenv("DS_LOCAL_N");

@@ -81,6 +81,10 @@ struct ModeFixed {
         L = ceil_u32_clamped(ldexp(lo, frac));
         H = ceil_u32_clamped(ldexp(hi, frac));
     }
+    // every heavy result t_u + w with t_u >= L lands at or beyond H
+    __device__ __forceinline__ static bool heavy_beyond(D L, D H, double, double, unsigned long long minW) {
+        return (unsigned long long)L + minW >= (unsigned long long)H;
+    }
 };
 
 struct __align__(16) EdgeF64 {
@@ -118,6 +122,10 @@ struct ModeF64 {
     __device__ __forceinline__ static void window(double lo, double hi, int, D& L, D& H) {
         L = (D)__double_as_longlong(lo);
         H = (D)__double_as_longlong(hi);
+    }
+    // fl(t_u + w) >= fl(lo + min w) >= hi for every t_u >= lo (monotone rounding)
+    __device__ __forceinline__ static bool heavy_beyond(D, D, double lo, double hi, unsigned long long minW) {
+        return __dadd_rn(lo, __longlong_as_double((long long)minW)) >= hi;
     }
 };
 
@@ -226,7 +234,7 @@ struct Ctl {
     // standalone launch (k_big_relax) and is relaunched where it left off
     unsigned long long rs_pos, rs_req, rs_E, rs_Rc;
     unsigned long long rs_st, rs_phases, rs_visited, rs_escanned, rs_nbar, rs_npull;
-    unsigned long long rs_re, rs_scount, rs_old_scount, rs_pp, rs_bpar;
+    unsigned long long rs_re, rs_scount, rs_old_scount, rs_pp, rs_bpar, rs_hset;
     long long rs_idx;
     StepSlot xslot;  // results of the standalone push
     StepSlot lslot[2];  // block-local mode (CTA 0 alone)
@@ -269,6 +277,13 @@ struct KParams {
     unsigned long long local_edges, local_entries;  // SMALL kernel: CTA-0-only steps below these
     long long ceiling;
     unsigned long long timeout_ns;
+    // direction-optimised heavy step: pull into the unsettled rows when the
+    // push over S would stream more edges (symmetric graphs)
+    int hpull;
+    float hpull_ratio;
+    unsigned long long hpull_min;
+    unsigned long long nH;
+    unsigned long long min_heavy;  // smallest heavy weight: fixed W, or f64 bits
     const long long* indptr;  // original CSR row offsets (for m_r)
     const long long* Lptr;
     const Edge* Ledges;
@@ -594,10 +609,14 @@ __device__ __forceinline__ void load_run<unsigned long long>(const unsigned long
 // RANGE capture: bucket extraction by a dense scan of the distance array.
 // Also retires the previous bucket's S bits (atomicAnd: disjoint from the
 // new bucket's S, which only holds vertices with values >= the old hi).
-template <class M, bool SUM = false>
+// UNSET: instead capture every row whose value is >= L (unsettled, INF
+// included) over `ptr`, with the row's solver id as the entry value -- the
+// rows a heavy pull gathers into (see pull_gather in relax_step).
+template <class M, bool SUM = false, bool UNSET = false>
 __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                               typename M::D L, typename M::D H, int* S, unsigned long long* s_counter,
-                              unsigned long long n_scan, const int* old_S, unsigned long long old_count) {
+                              unsigned long long n_scan, const int* old_S, unsigned long long old_count,
+                              const long long* ptr) {
     using D = typename M::D;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem<D>& ws = sm.w[wib];
@@ -626,11 +645,15 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
 #pragma unroll
         for (int j = 0; j < kRangePer; ++j) {
             const D d = dv[j];
+            if (UNSET) {
+                if (d >= L && v0 + j < n) hits |= 1u << j;
+                continue;
+            }
             if (d >= H && d != M::INF && (unsigned long long)d < cmin) cmin = (unsigned long long)d;
             if (d >= L && d < H) hits |= 1u << j;
         }
         if (cmin < local_min) local_min = cmin;
-        if (SUM) {  // exact bound for the chunk (no relaxation runs during this step)
+        if (SUM && !UNSET) {  // exact bound for the chunk (no relaxation runs during this step)
             cmin = warp_min(cmin);
             if (lane == 0) p.csum[c] = cmin == ~0ull ? M::INF : (D)cmin;
         }
@@ -652,11 +675,15 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
                     const int b = __ffs(rem) - 1;
                     rem &= rem - 1;
                     vtx[j] = (int)(v0 + b);
-                    // select, not dv[b]: a dynamic index would move dv[] to local memory
-                    D x = dv[0];
+                    if (UNSET) {
+                        cd[j] = (D)(v0 + b);  // the entry carries the row id
+                    } else {
+                        // select, not dv[b]: a dynamic index would move dv[] to local memory
+                        D x = dv[0];
 #pragma unroll
-                    for (int i = 1; i < kRangePer; ++i) x = (b == i) ? dv[i] : x;
-                    cd[j] = x;
+                        for (int i = 1; i < kRangePer; ++i) x = (b == i) ? dv[i] : x;
+                        cd[j] = x;
+                    }
                 }
             }
             bool news[kListPer];
@@ -664,20 +691,23 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
             for (int j = 0; j < kListPer; ++j) {
                 const bool in = vtx[j] >= 0;
                 if (in) {
-                    off[j] = __ldg(p.Lptr + vtx[j]);
-                    deg[j] = __ldg(p.Lptr + vtx[j] + 1) - off[j];
+                    off[j] = __ldg(ptr + vtx[j]);
+                    deg[j] = __ldg(ptr + vtx[j] + 1) - off[j];
                 }
-                news[j] = in && claim_bit(p.sbits, (unsigned)vtx[j]);
+                news[j] = !UNSET && in && claim_bit(p.sbits, (unsigned)vtx[j]);
             }
+            if (!UNSET) {
 #pragma unroll
-            for (int j = 0; j < kListPer; ++j)
-                wq_push<D, false>(ws.q, queue_vals(ws), qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
+                for (int j = 0; j < kListPer; ++j)
+                    wq_push<D, false>(ws.q, queue_vals(ws), qn, news[j], vtx[j], (D)0, lane, S, nullptr,
+                                      s_counter);
+            }
             capture_emit<M, kListPer>(p, slot, lane, cd, off, deg);
         }
-        if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
+        if (!UNSET && (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2))
             wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
     };
-    if (SUM) {
+    if (SUM && !UNSET) {
         // the warp's chunks are the usual grid-strided ones; each lane reads the
         // bound of one of them (one round trip for up to 32 chunks) and the
         // warp scans only the chunks whose bound is below hi.  Every stored value >= lo of a chunk is >= its
@@ -700,6 +730,7 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
     } else {
         for (unsigned long long c = gw; c < nchunk; c += nw) scan_chunk(c);
     }
+    if (UNSET) return;  // the entry / edge totals are in slot->re_packed
     wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
     const unsigned long long fc = block_reduce<0>(local_fc, sm.red);
     const unsigned long long mn = block_reduce<1>(local_min, sm.red2);
@@ -788,7 +819,13 @@ __device__ __forceinline__ void csum_lower(const KParams<M>& p, unsigned v, type
 
 // SUM: also lower the scan-chunk bound of every target that may have received
 // a value beyond the window (SMALL kernel, see capture_range).
-template <class M, bool LIGHT, bool LOCALW = false, bool SUM = false>
+// PULL (heavy only): the entries are the UNSETTLED rows v (capture_range
+// UNSET, entry value = v) and every edge v->u of A_H (= A_H^T, symmetric
+// graphs) gathers t[u] + w when u is settled (t[u] < H): the reference's own
+// pulled form of the heavy relaxation, r = A_H^T (t o S) (sssp.py:206-227),
+// restricted to the rows it can still lower.  See the direction choice at
+// POS_HEAVY for why this is exact.
+template <class M, bool LIGHT, bool LOCALW = false, bool SUM = false, bool PULL = false>
 __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                            unsigned long long E, unsigned long long Rc,
                            const typename M::Edge* edges, typename M::D H, int* out_list,
@@ -961,6 +998,36 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         }
 #define DS_DU(j) ws.d[kk[j]]
 #endif
+        if constexpr (PULL) {
+            // gather: source value t[u] (settled iff < H; settled values are
+            // final, so an L1 copy is exact) and the row's own value (a stale
+            // copy is >= the current one: at worst a redundant atomic)
+            D du[kRelPer], cur[kRelPer];
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                du[j] = M::INF;
+                cur[j] = (D)0;
+                if (32 * j < left) {
+                    du[j] = p.dist[M::col(ed[j])];
+                    cur[j] = p.dist[(unsigned)DS_DU(j)];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                if (32 * j < left && du[j] < H) {
+                    D nd;
+                    if (!M::add(du[j], ed[j], nd)) {
+                        overflow = true;
+                    } else if (nd < cur[j]) {
+                        const unsigned v = (unsigned)DS_DU(j);
+                        atomicMin(p.dist + v, nd);
+                        if (SUM) csum_lower(p, v, nd);
+                    }
+                }
+            }
+            __syncwarp();
+            continue;
+        }
         if (LIGHT && DS_DEFER_APPEND) drain();  // previous chunk's claims, edges in flight
         D nd[kRelPer], cur[kRelPer];
 #pragma unroll
@@ -1277,6 +1344,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     long long idx = 0;
     unsigned long long phases = 0, visited = 0;
     unsigned long long re = 0, scount = 0, old_scount = 0;
+    unsigned long long hset = 0;  // heavy edges of the rows settled so far
     int pp = 0;
     unsigned bpar = 0;
     int pos = POS_BUCKET;
@@ -1294,6 +1362,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         old_scount = ldcg(&c->rs_old_scount);
         pp = (int)ldcg(&c->rs_pp);
         bpar = (unsigned)ldcg(&c->rs_bpar);
+        hset = ldcg(&c->rs_hset);
         pos = pos0;
         resumed = true;
     }
@@ -1336,6 +1405,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             c->rs_old_scount = old_scount;
             c->rs_pp = (unsigned long long)pp;
             c->rs_bpar = bpar;
+            c->rs_hset = hset;
             StepSlot* x = &c->xslot;
             x->re_packed = x->front_count = x->append_count = 0;
             x->flags = 0;
@@ -1358,7 +1428,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
             if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[bpar ^ 1] = 0;
             capture_range<M, kSum>(p, sm, &c->slot[st % 3], L, H, p.S[bpar], &c->s_count[bpar],
-                             (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount);
+                             (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount, p.Lptr);
             old_scount = 0;
             if (!end_step(0, (unsigned long long)n_scan)) return;
             const unsigned long long fc = ldcg(&prev()->front_count);
@@ -1565,11 +1635,46 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 re = ldcg(&prev()->re_packed);
             }
             const unsigned long long E = heavy_done ? 0ull : (re & kMask33);
-            if (E >= p.big_heavy) {
+            hset += re & kMask33;  // S's rows are settled: their heavy edges leave the pull volume
+            // ---- direction choice.  The push streams E = |A_H rows of S|; the
+            // pull streams only the rows that can still change (t >= H), whose
+            // heavy edges are U = nnz(A_H) - (heavy edges of every settled row).
+            // Exactness of the pull (same t afterwards as the push):
+            //  * heavy_beyond: every t_u + w (t_u >= L, w heavy) is >= H, so
+            //    the step changes no value below H -- S's values are fixed
+            //    during it (the push reads them captured; the pull live) and
+            //    rows below H cannot receive anything;
+            //  * gating on t_u < H selects S plus rows settled in earlier
+            //    buckets, whose t_u + w were applied then (no-ops now);
+            //  * rows >= H are the only possible targets; min is order-free.
+            if (!heavy_done && E > 0 && p.hpull && E >= p.hpull_min) {
+                const unsigned long long U = p.nH > hset ? p.nH - hset : 0ull;
+                if ((double)E > (double)p.hpull_ratio * (double)U &&
+                    M::heavy_beyond(L, H, lo, hi, p.min_heavy)) {
+                    capture_range<M, false, true>(p, sm, &c->slot[st % 3], H, M::INF, nullptr, nullptr,
+                                                  (unsigned long long)n_scan, nullptr, 0ull, p.Hptr);
+                    if (!end_step(11, (unsigned long long)n_scan)) return;
+                    const unsigned long long pre = ldcg(&prev()->re_packed);
+                    const unsigned long long Ep = pre & kMask33;
+                    ++npull;
+                    if (Ep > 0) {
+                        escanned += Ep;
+                        relax_step<M, false, false, kSum, true>(p, sm, &c->slot[st % 3], Ep, pre >> kPackShift,
+                                                                p.Hedges, H, nullptr, nullptr);
+                        if (!end_step(12, Ep)) return;
+                        if (ldcg(&prev()->flags) & 1u) {
+                            status = kDevOverflow;
+                            break;
+                        }
+                    }
+                    heavy_done = true;
+                }
+            }
+            if (heavy_done) {
+            } else if (E >= p.big_heavy) {
                 handoff(POS_AFTER_HEAVY, p.heavy_pull ? 3 : 2, E, re >> kPackShift);
                 return;
-            }
-            if (DS_PULL_HEAVY && E > pullH) {
+            } else if (DS_PULL_HEAVY && E > pullH) {
                 escanned += (unsigned long long)p.Hpull.nnz;
                 ++npull;
                 const unsigned sl = (unsigned)(st % 3);

@@ -11,7 +11,7 @@ indptr, _, _ = g.download()
 s = graphs.pick_sources(indptr, 1, seed=7)[0]
 g.solve(s, delta)
 st = g.solve(s, delta)
-names = ["scan", "l_relax", "l_capt", "h_capt", "h_relax", "l_pull", "l_commit", "h_pull", "h_commit", "l_local", "h_local"]
+names = ["scan", "l_relax", "l_capt", "h_capt", "h_relax", "l_pull", "l_commit", "h_pull", "h_commit", "l_local", "h_local", "u_capt", "h_gather"]
 cap = 1 << 16
 buf = np.zeros(1 + 2 * cap, dtype=np.uint64)
 m = _lib.lib().ds_debug_trace(g._handle(), buf.ctypes.data, cap)
