@@ -52,7 +52,10 @@ def _stale(lib: str) -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIB_DIR, exist_ok=True)
+    only_main = os.environ.get("DS_BUILD_MAIN_ONLY") == "1"  # quick iteration builds
     for lib, extra in VARIANTS.items():
+        if only_main and lib != LIB:
+            continue
         if not force and not _stale(lib):
             continue
         tmp = lib + ".tmp"

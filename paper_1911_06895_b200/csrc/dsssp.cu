@@ -248,6 +248,7 @@ struct ds_graph {
     void* csum = nullptr;  // scan-chunk bounds (SMALL kernel)
     int* order = nullptr;  // solver id -> input id
     int* perm = nullptr;   // input id -> solver id
+    unsigned* sdeg = nullptr;  // solver id -> out-degree in A (for m_r at finalize)
     long long n_active = 0;
     Ctl* ctl = nullptr;
     Ctl* h_ctl = nullptr;  // host mirror
@@ -314,7 +315,7 @@ static void free_all(ds_graph* g) {
                     g->dist,   g->fbits, g->sbits, g->F0,  g->F1,  g->Fv0, g->Fv1, g->S0, g->S1, g->req, g->Rpre,
                     g->planL.rowid, g->planL.cptr, g->planL.chunk_row, g->planL.span,
                     g->planH.rowid, g->planH.cptr, g->planH.chunk_row, g->planH.span,
-                    g->Rbase,  g->Rd,   g->chunk_start, g->order, g->perm, g->ctl,
+                    g->Rbase,  g->Rd,   g->chunk_start, g->order, g->perm, g->sdeg, g->ctl,
                     g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace, g->csum};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -618,10 +619,12 @@ __global__ void k_indeg_key(const int* col, long long nnz, unsigned* key) {
 }
 
 __global__ void k_invert_order(const int* order, const unsigned* skey, long long n, int* perm,
-                               long long* n_active) {
+                               long long* n_active, const long long* indptr, unsigned* sdeg) {
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
          r += (long long)gridDim.x * blockDim.x) {
-        perm[order[r]] = (int)r;
+        const int v = order[r];
+        perm[v] = (int)r;
+        sdeg[r] = (unsigned)(indptr[v + 1] - indptr[v]);  // out-degree in solver order (m_r)
         if (skey[r] > 0 && (r + 1 == n || skey[r + 1] == 0)) *n_active = r + 1;
     }
 }
@@ -1050,6 +1053,7 @@ static int compute_order(ds_graph* g) {
     } while (0)
     CKO(cudaMalloc(&g->order, sizeof(int) * n));
     CKO(cudaMalloc(&g->perm, sizeof(int) * n));
+    if (!g->sdeg) CKO(cudaMalloc(&g->sdeg, sizeof(unsigned) * n));
     CKO(cudaMalloc(&key, sizeof(unsigned) * n));
     CKO(cudaMalloc(&skey, sizeof(unsigned) * n));
     CKO(cudaMalloc(&iota, sizeof(int) * n));
@@ -1064,7 +1068,8 @@ static int compute_order(ds_graph* g) {
     if (rc) return done(rc);
     CKO(cub::DeviceRadixSort::SortPairsDescending(g->cub_tmp, bytes, key, skey, iota, g->order, n, 0,
                                                   32, g->stream));
-    k_invert_order<<<elementwise_grid(g), 256, 0, g->stream>>>(g->order, skey, n, g->perm, nact);
+    k_invert_order<<<elementwise_grid(g), 256, 0, g->stream>>>(g->order, skey, n, g->perm, nact, g->indptr,
+                                                               g->sdeg);
     CKO(cudaGetLastError());
     CKO(cudaMemcpyAsync(&g->n_active, nact, sizeof(long long), cudaMemcpyDeviceToHost, g->stream));
     CKO(cudaStreamSynchronize(g->stream));
@@ -1504,6 +1509,7 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     p.chunk_start = x.chunk_start;
     p.csum = (typename M::D*)x.csum;
     p.perm = g->perm;
+    p.sdeg = g->sdeg;
     p.n_active = g->n_active;
     p.ctl = x.ctl;
     p.out = x.out;
@@ -1589,6 +1595,15 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     if (trace) {
         g->trace_len = std::min(c.steps, g->trace_cap);
         g->trace_t0 = c.last_bucket;
+        if (c.t_enter && c.t_exit && c.steps > 0) {
+            // init = entry -> first step start; finalize = last step end -> last CTA done
+            unsigned long long last[2] = {0, 0};
+            const unsigned long long k = std::min(c.steps, g->trace_cap) - 1;
+            if (cudaMemcpy(last, g->trace + 2 * k, sizeof(last), cudaMemcpyDeviceToHost) == cudaSuccess)
+                fprintf(stderr, "[ds trace] init %.1f us, finalize %.1f us\n",
+                        (double)(c.last_bucket - (long long)c.t_enter) / 1e3,
+                        (double)(c.t_exit - last[0]) / 1e3);
+        }
     }
     *dev_status = c.status;
     return DS_OK;

@@ -243,6 +243,7 @@ struct Ctl {
     // by CTA 0 racing ahead into the local heavy step
     unsigned long long h_phases, h_re, h_pp, h_done, h_status, h_escanned;
     unsigned long long hh_re, hh_done, hh_status;
+    unsigned long long t_enter, t_exit;  // DS_TRACE: kernel entry / last CTA's finalize end
 };
 
 enum : int { POS_FRESH = 0, POS_BUCKET = 1, POS_PHASE = 2, POS_AFTER_LIGHT = 3, POS_HEAVY = 4,
@@ -303,6 +304,7 @@ struct KParams {
     D* Rd;
     unsigned* chunk_start;
     const int* perm;      // input id -> solver id (degree-sorted relabeling)
+    const unsigned* sdeg; // solver id -> out-degree in A (m_r)
     long long n_active;   // solver ids >= n_active have no edges at all
     Ctl* ctl;
     double* out;
@@ -1301,6 +1303,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     unsigned gen = 0;
     unsigned long long deadline = 0;
     const int pos0 = (int)ldcg(&c->rs_pos);
+    if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && pos0 == POS_FRESH) c->t_enter = globaltimer_ns();
     if (threadIdx.x == 0) {
         deadline = globaltimer_ns() + p.timeout_ns;
         // resumed launches continue the barrier sequence
@@ -1732,17 +1735,51 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             const unsigned v = (unsigned)ldcg(p.S[bpar ^ 1] + i);
             atomicAnd(p.sbits + (v >> 5), ~(1u << (v & 31)));
         }
+        // 8 vertices per thread and round: independent loads in flight (a
+        // one-per-thread loop is a chain of dependent round trips)
         unsigned long long cnt = 0, m = 0, mx = 0;
-        const long long stride = (long long)gridDim.x * kThreads;
-        for (long long v = (long long)blockIdx.x * kThreads + threadIdx.x; v < p.n; v += stride) {
-            const long long sv = __ldg(p.perm + v);
-            const D d = sv < n_scan ? __ldcg(p.dist + sv) : M::INF;
-            if (d != M::INF) {
-                ++cnt;
-                m += (unsigned long long)(__ldg(p.indptr + v + 1) - __ldg(p.indptr + v));
-                if ((unsigned long long)d > mx) mx = (unsigned long long)d;
+        const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
+        const long long stride8 = 8ll * gridDim.x * kThreads;
+        for (long long v0 = 8 * tid; v0 < p.n; v0 += stride8) {
+            int sv[8];
+            const bool full = v0 + 8 <= p.n;
+            if (full) {
+                const int4 a = __ldg(reinterpret_cast<const int4*>(p.perm + v0));
+                const int4 b = __ldg(reinterpret_cast<const int4*>(p.perm + v0) + 1);
+                sv[0] = a.x; sv[1] = a.y; sv[2] = a.z; sv[3] = a.w;
+                sv[4] = b.x; sv[5] = b.y; sv[6] = b.z; sv[7] = b.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) sv[j] = v0 + j < p.n ? __ldg(p.perm + v0 + j) : (int)n_scan;
             }
-            p.out[v] = M::to_f64(d, p.frac);
+            D d[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) d[j] = sv[j] < n_scan ? __ldcg(p.dist + sv[j]) : M::INF;
+            double o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (d[j] != M::INF) {
+                    ++cnt;
+                    if ((unsigned long long)d[j] > mx) mx = (unsigned long long)d[j];
+                }
+                o[j] = M::to_f64(d[j], p.frac);
+            }
+            if (full) {
+                double2* q = reinterpret_cast<double2*>(p.out + v0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) q[j] = make_double2(o[2 * j], o[2 * j + 1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (v0 + j < p.n) p.out[v0 + j] = o[j];
+            }
+        }
+        // m_r = sum of out-degrees of the reached vertices, in solver order
+        for (long long s0 = 8 * tid; s0 < n_scan; s0 += stride8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (s0 + j < n_scan && __ldcg(p.dist + s0 + j) != M::INF) m += __ldg(p.sdeg + s0 + j);
+            }
         }
         cnt = block_reduce<0>(cnt, sm.red);
         m = block_reduce<0>(m, sm.red2);
@@ -1751,6 +1788,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             atomicAdd(&c->reached, cnt);
             atomicAdd(&c->edges_reached, m);
             atomicMax(&c->max_d, mx);
+            if (p.trace) atomicMax(&c->t_exit, globaltimer_ns());
             if (blockIdx.x == 0) {
                 c->phases = phases;
                 c->visited = visited;
