@@ -1336,6 +1336,9 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
         per = q > 4e18 ? (LLONG_MAX / 4) : (long long)q + 2;
     }
     g->ceiling = per > LLONG_MAX / n ? LLONG_MAX : n * per;
+    // test hook: a small ceiling makes the reference's non-convergence error
+    // path (sssp.py:296-301) reachable on ordinary graphs
+    if (const char* e = getenv("DS_CEILING_OVERRIDE")) g->ceiling = atoll(e);
     // the push's shared-memory row bases are 32-bit edge indices
     if (g->nL >= (1LL << 32) || g->nH >= (1LL << 32))
         return set_err(DS_EINVAL, "light or heavy edge count %lld exceeds 2^32",
@@ -1435,9 +1438,13 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     p.delta = g->delta;
     p.frac = g->frac;
     p.ceiling = g->ceiling;
-    double tmo = 120.0;
+    double tmo;
+    // The device watchdog is opt-in (the reference has no time limit, so a
+    // valid long solve must not become an error): DS_TIMEOUT_S=seconds arms
+    // it (tests and probes set it so a bad build cannot hang the device).
+    tmo = 0.0;
     if (const char* s = getenv("DS_TIMEOUT_S")) tmo = atof(s);
-    p.timeout_ns = (unsigned long long)(tmo * 1e9);
+    p.timeout_ns = tmo > 0 ? (unsigned long long)(tmo * 1e9) : ~0ull;
     p.indptr = g->indptr;
     p.Lptr = g->Lptr;
     p.Ledges = (const typename M::Edge*)g->Ledges;
@@ -1558,6 +1565,9 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
             CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M, true>, p));
         else
             CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M, false>, p));
+        // end of the device work so far (re-recorded after a resumed launch):
+        // kernel_ms excludes the host's wake-up after the synchronize below
+        CK(cudaEventRecord(x.ev1, x.stream));
         CK(cudaMemcpyAsync(x.h_ctl, x.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, x.stream));
         CK(cudaStreamSynchronize(x.stream));
         const Ctl& h = *x.h_ctl;
@@ -1576,8 +1586,6 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         }
         CK(cudaGetLastError());
     }
-    CK(cudaEventRecord(x.ev1, x.stream));
-    CK(cudaStreamSynchronize(x.stream));
     const Ctl& c = *x.h_ctl;
     // an interrupted solve may leave dedup bits set: clear them for the next one
     if (c.abort || c.status != 0) {

@@ -1305,7 +1305,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     const int pos0 = (int)ldcg(&c->rs_pos);
     if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && pos0 == POS_FRESH) c->t_enter = globaltimer_ns();
     if (threadIdx.x == 0) {
-        deadline = globaltimer_ns() + p.timeout_ns;
+        const unsigned long long now = globaltimer_ns();
+        deadline = p.timeout_ns > ~0ull - now ? ~0ull : now + p.timeout_ns;  // saturating: ~0 = unarmed
         // resumed launches continue the barrier sequence
 #if DS_BARRIER == 1
         gen = (unsigned)(ldcg(&c->bar_arrive) / gridDim.x);

@@ -17,6 +17,7 @@ Reference interface mirrored (file:line under /root/reference/pkg/src/deltaspars
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import math
 import threading
@@ -81,6 +82,29 @@ def bucket_bounds(index: int, delta: float) -> tuple[float, float]:
     return index * delta, (index + 1) * delta
 
 
+def _check_out(a, count: int, dtype, name: str) -> None:
+    """Caller-provided output buffers are written through raw pointers: reject
+    a wrong dtype, a non-contiguous layout or fewer than `count` elements
+    instead of overrunning them."""
+    dt = np.dtype(dtype)
+    if hasattr(a, "data_ptr"):  # torch tensor
+        if str(a.dtype).replace("torch.", "") != dt.name:
+            raise ValueError(f"{name} must be {dt.name}, got {a.dtype}")
+        if not a.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if a.numel() < count:
+            raise ValueError(f"{name} holds {a.numel()} elements, needs {count}")
+        return
+    if not isinstance(a, np.ndarray):
+        raise ValueError(f"{name} must be a numpy array or a torch tensor")
+    if a.dtype != dt:
+        raise ValueError(f"{name} must be {dt.name}, got {a.dtype}")
+    if not a.flags.c_contiguous:
+        raise ValueError(f"{name} must be C-contiguous")
+    if a.size < count:
+        raise ValueError(f"{name} holds {a.size} elements, needs {count}")
+
+
 def _ptr(a) -> int:
     if a is None:
         return 0
@@ -117,6 +141,13 @@ class DeviceGraph:
         self.device = int(device)
         self.last_stats: _lib.Stats | None = None
         self.prep: _lib.PrepInfo | None = None
+        # A ds_graph handle is not re-entrant (include/dsssp.h): calls that
+        # touch its scratch hold this lock (ctypes releases the GIL).  The
+        # reference promises that concurrent invocations on a shared
+        # immutable graph are safe; they serialise here.
+        self.lock = threading.RLock()
+        self._users = 0        # cached handles: callers currently using it
+        self._evicted = False  # dropped from the cache; closed by the last user
 
     # -- construction ---------------------------------------------------
     @classmethod
@@ -170,14 +201,16 @@ class DeviceGraph:
         return self._h
 
     def set_stream(self, stream: int | None) -> None:
-        _lib.check(_lib.lib().ds_graph_set_stream(self._handle(), stream or 0))
+        with self.lock:
+            _lib.check(_lib.lib().ds_graph_set_stream(self._handle(), stream or 0))
 
     def prepare(self, delta: float, force_f64: bool = False) -> _lib.PrepInfo:
         info = _lib.PrepInfo()
         flags = _lib.DS_FLAG_FORCE_F64 if force_f64 else 0
-        _lib.check(_lib.lib().ds_graph_prepare(self._handle(), float(delta), flags,
-                                               ctypes.byref(info)))
-        self.prep = info
+        with self.lock:
+            _lib.check(_lib.lib().ds_graph_prepare(self._handle(), float(delta), flags,
+                                                   ctypes.byref(info)))
+            self.prep = info
         return info
 
     def solve(self, source: int, delta: float, skip_empty_buckets: bool = False,
@@ -185,9 +218,10 @@ class DeviceGraph:
         st = _lib.Stats()
         flags = (_lib.DS_FLAG_SKIP_EMPTY if skip_empty_buckets else 0) | (
             _lib.DS_FLAG_FORCE_F64 if force_f64 else 0)
-        _lib.check(_lib.lib().ds_sssp(self._handle(), int(source), float(delta), flags,
-                                      ctypes.byref(st)))
-        self.last_stats = st
+        with self.lock:
+            _lib.check(_lib.lib().ds_sssp(self._handle(), int(source), float(delta), flags,
+                                          ctypes.byref(st)))
+            self.last_stats = st
         return st
 
     def solve_batch(self, sources, delta: float, skip_empty_buckets: bool = False,
@@ -207,54 +241,72 @@ class DeviceGraph:
             dptr, dist = out, None
         else:
             dist = out if out is not None else np.empty((k, self.n), dtype=np.float64)
+            _check_out(dist, k * self.n, np.float64, "out")
             dptr = _ptr(dist)
-        _lib.check(_lib.lib().ds_sssp_batch(self._handle(), _ptr(src), k, float(delta), flags,
-                                            int(concurrency), stats, dptr))
-        self.last_stats = None
+        with self.lock:
+            _lib.check(_lib.lib().ds_sssp_batch(self._handle(), _ptr(src), k, float(delta), flags,
+                                                int(concurrency), stats, dptr))
+            self.last_stats = None
         return [stats[i] for i in range(k)], dist
 
     def result_dense(self, out=None) -> np.ndarray:
         if out is None:
             out = np.empty(self.n, dtype=np.float64)
-        _lib.check(_lib.lib().ds_result_dense(self._handle(), _ptr(out)))
+        _check_out(out, self.n, np.float64, "out")
+        with self.lock:
+            _lib.check(_lib.lib().ds_result_dense(self._handle(), _ptr(out)))
         return out
 
     def result_sparse(self, out=None):
         """(indices int64, values float64) of reached vertices; `out` may be a
         pair of preallocated (pinned) buffers with >= reached entries."""
-        r = int(self.last_stats.reached) if self.last_stats is not None else self.n
-        if out is None:
-            idx = np.empty(r, dtype=np.int64)
-            val = np.empty(r, dtype=np.float64)
-        else:
-            idx, val = out[0][:r], out[1][:r]
-        _lib.check(_lib.lib().ds_result_sparse(self._handle(), _ptr(idx), _ptr(val)))
+        with self.lock:
+            r = int(self.last_stats.reached) if self.last_stats is not None else self.n
+            if out is None:
+                idx = np.empty(r, dtype=np.int64)
+                val = np.empty(r, dtype=np.float64)
+            else:
+                _check_out(out[0], r, np.int64, "out[0]")
+                _check_out(out[1], r, np.float64, "out[1]")
+                idx, val = out[0][:r], out[1][:r]
+            _lib.check(_lib.lib().ds_result_sparse(self._handle(), _ptr(idx), _ptr(val)))
         return idx, val
 
     def export_split(self, which: int):
         """Light (0) / heavy (1) CSR of the current prepare as host arrays."""
-        if self.prep is None:
-            raise ValueError("export_split needs a prepare() first")
-        m = int(self.prep.nnz_heavy if which else self.prep.nnz_light)
-        indptr = np.empty(self.n + 1, dtype=np.int64)
-        col = np.empty(max(m, 1), dtype=np.int64)
-        val = np.empty(max(m, 1), dtype=np.float64)
-        _lib.check(_lib.lib().ds_export_split(self._handle(), int(which), _ptr(indptr), _ptr(col),
-                                              _ptr(val)))
+        with self.lock:
+            if self.prep is None:
+                raise ValueError("export_split needs a prepare() first")
+            m = int(self.prep.nnz_heavy if which else self.prep.nnz_light)
+            indptr = np.empty(self.n + 1, dtype=np.int64)
+            col = np.empty(max(m, 1), dtype=np.int64)
+            val = np.empty(max(m, 1), dtype=np.float64)
+            _lib.check(_lib.lib().ds_export_split(self._handle(), int(which), _ptr(indptr), _ptr(col),
+                                                  _ptr(val)))
         return indptr, col[:m], val[:m]
 
-    def download(self):
-        """Original CSR (int64 indptr, int32 col, float32 val) to host."""
-        indptr = np.empty(self.n + 1, dtype=np.int64)
-        col = np.empty(max(self.nnz, 1), dtype=np.int32)
-        val = np.empty(max(self.nnz, 1), dtype=np.float32)
-        _lib.check(_lib.lib().ds_graph_download(self._handle(), _ptr(indptr), _ptr(col), _ptr(val)))
+    def download(self, out=None):
+        """Original CSR (int64 indptr, int32 col, float32 val), to host arrays
+        or into `out` = (indptr, col, val) buffers (numpy, or torch tensors on
+        the graph's device: no host round trip)."""
+        if out is None:
+            indptr = np.empty(self.n + 1, dtype=np.int64)
+            col = np.empty(max(self.nnz, 1), dtype=np.int32)
+            val = np.empty(max(self.nnz, 1), dtype=np.float32)
+        else:
+            indptr, col, val = out
+            _check_out(indptr, self.n + 1, np.int64, "indptr")
+            _check_out(col, self.nnz, np.int32, "col")
+            _check_out(val, self.nnz, np.float32, "val")
+        with self.lock:
+            _lib.check(_lib.lib().ds_graph_download(self._handle(), _ptr(indptr), _ptr(col), _ptr(val)))
         return indptr, col[: self.nnz], val[: self.nnz]
 
     def close(self) -> None:
-        if self._h.value:
-            _lib.lib().ds_graph_destroy(self._h)
-            self._h = ctypes.c_void_p()
+        with self.lock:
+            if self._h.value:
+                _lib.lib().ds_graph_destroy(self._h)
+                self._h = ctypes.c_void_p()
 
     def __del__(self):
         try:
@@ -274,26 +326,46 @@ _CACHE_SIZE = 2
 _CACHE_LOCK = threading.Lock()
 
 
+def _retire(g: DeviceGraph) -> None:
+    """Drop a cached handle: closed now if idle, else by its last user."""
+    g._evicted = True
+    if g._users == 0:
+        g.close()
+
+
 def clear_device_cache() -> None:
     with _CACHE_LOCK:
         for _, g in _CACHE.values():
-            g.close()
+            _retire(g)
         _CACHE.clear()
 
 
-def _device_graph(matrix, device: int = 0) -> DeviceGraph:
+@contextlib.contextmanager
+def _device_graph(matrix, device: int = 0):
+    """The cached device copy of `matrix`, pinned for the duration of the
+    `with` block: eviction by another thread (or clear_device_cache) defers
+    the close until every user has left, so no call ever runs on a freed
+    handle."""
     key = id(matrix)
     with _CACHE_LOCK:
         hit = _CACHE.get(key)
         if hit is not None and hit[0] is matrix:
             _CACHE.move_to_end(key)
-            return hit[1]
-        g = DeviceGraph.from_matrix(matrix, device)
-        _CACHE[key] = (matrix, g)
-        while len(_CACHE) > _CACHE_SIZE:
-            _, (_, old) = _CACHE.popitem(last=False)
-            old.close()
-        return g
+            g = hit[1]
+        else:
+            g = DeviceGraph.from_matrix(matrix, device)
+            _CACHE[key] = (matrix, g)
+            while len(_CACHE) > _CACHE_SIZE:
+                _, (_, old) = _CACHE.popitem(last=False)
+                _retire(old)
+        g._users += 1
+    try:
+        yield g
+    finally:
+        with _CACHE_LOCK:
+            g._users -= 1
+            if g._evicted and g._users == 0:
+                g.close()
 
 
 # ------------------------------------------------------------------ API
@@ -322,9 +394,9 @@ def delta_stepping(
     if not (delta > 0) or not math.isfinite(delta):
         raise ValueError(f"delta must be a positive finite number, got {delta}")
     start = time.perf_counter()
-    g = _device_graph(matrix)
-    st = g.solve(int(source), float(delta), skip_empty_buckets=skip_empty_buckets)
-    idx, val = g.result_sparse()
+    with _device_graph(matrix) as g, g.lock:  # solve + fetch as one unit
+        st = g.solve(int(source), float(delta), skip_empty_buckets=skip_empty_buckets)
+        idx, val = g.result_sparse()
     elapsed = time.perf_counter() - start
     return SsspResult(
         distances=SparseVector(matrix.n, idx, val),
@@ -360,9 +432,9 @@ def delta_stepping_batch(
     if not srcs:
         return []
     start = time.perf_counter()
-    g = _device_graph(matrix)
-    stats, dist = g.solve_batch(srcs, float(delta), skip_empty_buckets=skip_empty_buckets,
-                                concurrency=concurrency)
+    with _device_graph(matrix) as g:
+        stats, dist = g.solve_batch(srcs, float(delta), skip_empty_buckets=skip_empty_buckets,
+                                    concurrency=concurrency)
     elapsed = (time.perf_counter() - start) / len(srcs)
     out = []
     for i, st in enumerate(stats):
@@ -383,10 +455,10 @@ def split_edges(matrix, delta: float, workers: int = 1, chunks_per_worker: int =
     kernels and returned as host `SparseMatrix` objects."""
     if not (delta > 0) or not math.isfinite(delta):
         raise ValueError(f"delta must be a positive finite number, got {delta}")
-    g = _device_graph(matrix)
-    g.prepare(float(delta))
     out = []
-    for which in (0, 1):
-        indptr, col, val = g.export_split(which)
-        out.append(SparseMatrix(matrix.n, indptr, col, val))
+    with _device_graph(matrix) as g, g.lock:
+        g.prepare(float(delta))
+        for which in (0, 1):
+            indptr, col, val = g.export_split(which)
+            out.append(SparseMatrix(matrix.n, indptr, col, val))
     return out[0], out[1]

@@ -14,6 +14,9 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(REPO, "tests", "golden")
 if REPO not in sys.path:
     sys.path.insert(0, REPO)
+# arm the device watchdog (opt-in in the library): a broken build fails a
+# test with DS_ETIMEOUT instead of hanging the GPU
+os.environ.setdefault("DS_TIMEOUT_S", "300")
 
 
 def pytest_configure(config):
