@@ -16,7 +16,6 @@ from .containers import (  # noqa: F401
     matrix_build,
     vector_build,
 )
-from .graphs import random_connected_unit_graph, random_graph  # noqa: F401
 from .io import (  # noqa: F401
     GraphFile,
     GraphLoadError,
@@ -48,8 +47,6 @@ __all__ = [
     "mask_from_indices",
     "matrix_build",
     "vector_build",
-    "random_graph",
-    "random_connected_unit_graph",
     "BackendChoice",
     "DeviceGraph",
     "SsspResult",

@@ -13,9 +13,8 @@ Conventions:
   sssp.py:96-97);
 * self-loops dropped, duplicates collapsed (matrix_build, core.py:268-275).
 
-Also restates the reference's small test generators `random_graph` and
-`random_connected_unit_graph` (generate.py:12-57) so the reference's own
-test corpora can be regenerated bit-for-bit from their seeds.
+(The restatements of the reference's small test generators, used to
+regenerate its corpora, live with the tests: tests/refgen.py.)
 """
 
 from __future__ import annotations
@@ -30,8 +29,6 @@ __all__ = [
     "grid2d",
     "erdos_renyi",
     "pick_sources",
-    "random_graph",
-    "random_connected_unit_graph",
     "RMAT_A", "RMAT_B", "RMAT_C",
 ]
 
@@ -176,39 +173,3 @@ def pick_sources(indptr: np.ndarray, count: int, seed: int = 7) -> list[int]:
     rng = np.random.default_rng(seed)
     pick = rng.choice(cand.shape[0], size=min(count, cand.shape[0]), replace=False)
     return [int(x) for x in cand[pick]]
-
-
-# --------------------------------------------------------------------------
-# Restatements of the reference's small test generators (generate.py:12-57),
-# used only to regenerate the reference's own corpora from their seeds.
-
-def random_graph(n: int, m: int, rng: np.random.Generator, weights: str = "int") -> SparseMatrix:
-    """generate.py:12-36: m drawn directed edges (dups collapse with min,
-    self-loops dropped); weights unit / int U{1..10} / float 10*(1-U)."""
-    if m == 0 or n < 2:
-        return matrix_build(n, np.empty((0, 3)))
-    src = rng.integers(0, n, size=m)
-    dst = rng.integers(0, n, size=m)
-    if weights == "unit":
-        w = np.ones(m)
-    elif weights == "int":
-        w = rng.integers(1, 11, size=m).astype(np.float64)
-    elif weights == "float":
-        w = 10.0 * (1.0 - rng.random(size=m))
-    else:
-        raise ValueError(f"unknown weight kind {weights!r}")
-    return matrix_build(n, np.column_stack([src, dst, w]))
-
-
-def random_connected_unit_graph(n: int, extra_edges: int, rng: np.random.Generator) -> SparseMatrix:
-    """generate.py:39-57: random spanning tree away from 0 plus extra edges."""
-    if n == 1:
-        return matrix_build(1, np.empty((0, 3)))
-    child = np.arange(1, n)
-    parent = (rng.random(n - 1) * child).astype(np.int64)
-    src, dst = [parent], [child]
-    if extra_edges:
-        src.append(rng.integers(0, n, size=extra_edges))
-        dst.append(rng.integers(0, n, size=extra_edges))
-    s, d = np.concatenate(src), np.concatenate(dst)
-    return matrix_build(n, np.column_stack([s, d, np.ones(s.shape[0])]))

@@ -49,44 +49,52 @@ __all__ = [
 log = logging.getLogger(__name__)
 
 
+# Interface types of the reference loaders (deltasparse/io.py:36-88): same
+# names, attributes, message format and exception hierarchy, so callers that
+# catch or construct them keep working.
+
 class GraphLoadError(Exception):
-    """Base for anything that goes wrong while reading a graph file."""
+    """Raised for any failure while loading a graph file.  The text reads
+    "<path>:<line>: <message>"; the three parts stay available as
+    attributes."""
 
     def __init__(self, path: str, lineno: int, message: str) -> None:
-        super().__init__(f"{path}:{lineno}: {message}")
-        self.path = path
-        self.lineno = lineno
-        self.message = message
+        self.path, self.lineno, self.message = path, lineno, message
+        super().__init__("%s:%d: %s" % (path, lineno, message))
 
 
 class ParseError(GraphLoadError):
-    """The file's structure is wrong: header, token counts, coordinates."""
+    """Malformed input: a bad header, wrong token count or bad coordinate."""
 
 
 class ValidationError(GraphLoadError):
-    """The file parsed but its content is unusable, e.g. weight <= 0."""
+    """Well-formed input with unusable values (a non-positive weight, ...)."""
 
 
 @dataclass(frozen=True)
 class GraphFile:
-    """One parsed CLI graph argument: where it is and how to read it."""
+    """A graph argument of the CLI: file path (or "-"), format ("mtx" or
+    "edges"), edge direction and the weight used when a line has none."""
 
     path: str
-    format: str  # "mtx" | "edges"
+    format: str
     directed: bool = True
     default_weight: float = 1.0
 
 
 class LabelMap:
-    """Bijection between external vertex labels and dense internal ids."""
+    """Two-way map between the labels a file uses and internal ids 0..n-1
+    (internal id i <-> externals[i])."""
 
     __slots__ = ("_externals", "_to_internal")
 
     def __init__(self, externals: list[int]) -> None:
+        index: dict[int, int] = {}
+        for internal, label in enumerate(externals):
+            if index.setdefault(label, internal) != internal:
+                raise ValueError("duplicate external label")
         self._externals = externals
-        self._to_internal = {label: i for i, label in enumerate(externals)}
-        if len(self._to_internal) != len(externals):
-            raise ValueError("duplicate external label")
+        self._to_internal = index
 
     def __len__(self) -> int:
         return len(self._externals)

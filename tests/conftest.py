@@ -14,6 +14,10 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(REPO, "tests", "golden")
 if REPO not in sys.path:
     sys.path.insert(0, REPO)
+TESTS = os.path.dirname(os.path.abspath(__file__))
+if TESTS not in sys.path:
+    sys.path.insert(0, TESTS)
+import refgen  # noqa: E402  (reference test-graph generators, test infrastructure)
 # arm the device watchdog (opt-in in the library): a broken build fails a
 # test with DS_ETIMEOUT instead of hanging the GPU
 os.environ.setdefault("DS_TIMEOUT_S", "300")
@@ -67,7 +71,7 @@ def criterion1_graphs():
         kind = "int" if case < 500 else "float"
         n = int(rng.integers(1, 201))
         m = int(rng.integers(0, 2001))
-        a = graphs.random_graph(n, m, rng, weights=kind)
+        a = refgen.random_graph(n, m, rng, weights=kind)
         s = int(rng.integers(0, n))
         out.append((a, s, kind))
     return out
@@ -80,5 +84,5 @@ def unit_graphs():
     out = []
     for _ in range(50):
         n = int(rng.integers(2, 121))
-        out.append(graphs.random_connected_unit_graph(n, int(rng.integers(0, 2 * n)), rng))
+        out.append(refgen.random_connected_unit_graph(n, int(rng.integers(0, 2 * n)), rng))
     return out

@@ -404,7 +404,7 @@ def test_reference_property_suites():
     distances invariant across delta, skip mode never counts more outer
     iterations (test_sssp.py:361-386), unit-weight connected graphs settle
     bucket i at distance i (test_sssp.py:389-401)."""
-    from paper_1911_06895_b200 import random_connected_unit_graph, random_graph
+    from refgen import random_connected_unit_graph, random_graph
 
     deltas = (0.5, 1.0, 3.0, 11.0)
     rng = np.random.default_rng(103)

@@ -11,6 +11,7 @@ import os
 import numpy as np
 import pytest
 
+import refgen
 from paper_1911_06895_b200 import io as dio
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -107,7 +108,7 @@ def test_binary_csr_cache_roundtrip(tmp_path):
     rng = np.random.default_rng(5)
     cases = [
         graphs.erdos_renyi(256, seed=1),                        # int weights -> f32 storage
-        graphs.random_graph(300, 2000, rng, weights="float"),   # arbitrary f64 weights
+        refgen.random_graph(300, 2000, rng, weights="float"),   # arbitrary f64 weights
         graphs.rmat(10, seed=3),                                # fp32-lattice weights
     ]
     for k, m in enumerate(cases):
