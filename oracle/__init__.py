@@ -54,6 +54,15 @@ def _load():
             _i64p, _i64p, _f64p, _i64p,
         ]
         lib.oracle_split.restype = ctypes.c_int
+        lib.oracle_rmat_build.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.c_int]
+        lib.oracle_rmat_build.restype = ctypes.c_void_p
+        lib.oracle_rmat_nnz.argtypes = [ctypes.c_void_p]
+        lib.oracle_rmat_nnz.restype = ctypes.c_int64
+        lib.oracle_rmat_fetch.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_rmat_fetch.restype = None
+        lib.oracle_rmat_free.argtypes = [ctypes.c_void_p]
+        lib.oracle_rmat_free.restype = None
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -139,3 +148,23 @@ def to_sparse(dist):
     the shape of the reference SparseVector (core.py:46-70)."""
     idx = np.flatnonzero(np.isfinite(dist)).astype(np.int64)
     return idx, dist[idx]
+
+
+def rmat(scale, edge_factor=16, seed=1, weight_seed=2, threads=0):
+    """Host R-MAT CSR (indptr int64, col int32, val float32), bit-identical to
+    paper_1911_06895_b200.graphs.rmat (restated in C with OpenMP in rmat.c) --
+    the reference arm's input without the product's CUDA library."""
+    lib = _load()
+    h = lib.oracle_rmat_build(int(scale), int(edge_factor), int(seed), int(weight_seed), int(threads))
+    if not h:
+        raise MemoryError("oracle R-MAT generation failed")
+    try:
+        nnz = int(lib.oracle_rmat_nnz(h))
+        n = 1 << int(scale)
+        indptr = np.empty(n + 1, dtype=np.int64)
+        col = np.empty(max(nnz, 1), dtype=np.int32)
+        val = np.empty(max(nnz, 1), dtype=np.float32)
+        lib.oracle_rmat_fetch(h, indptr.ctypes.data, col.ctypes.data, val.ctypes.data)
+    finally:
+        lib.oracle_rmat_free(h)
+    return indptr, col[:nnz], val[:nnz]

@@ -132,3 +132,17 @@ def test_threads_do_not_change_results():
         got = oracle.delta_stepping(g.n, g.indptr, g.col, g.val, 3, 0.1, threads=t)
         assert np.array_equal(got[0].view(np.uint64), base[0].view(np.uint64))
         assert got[1:] == base[1:]
+
+
+def test_host_rmat_generator_matches_graphs_rmat():
+    # the reference arm's input generator (oracle/rmat.c) must build exactly
+    # the CSR of graphs.rmat, which the device generator is pinned to as well
+    import oracle
+    from paper_1911_06895_b200 import graphs
+
+    for scale, ef, seed, wseed in [(6, 16, 1, 2), (11, 16, 1, 2), (14, 16, 1, 2), (12, 8, 5, 9)]:
+        ip, col, val = oracle.rmat(scale, ef, seed, wseed)
+        a = graphs.rmat(scale, ef, seed, wseed)
+        assert np.array_equal(ip, a.indptr)
+        assert np.array_equal(col, a.col)
+        assert np.array_equal(val.view(np.uint32), np.asarray(a.val, dtype=np.float32).view(np.uint32))
