@@ -20,10 +20,22 @@ grids (each source's result is exactly its single-source result).
             / mean kernel time vs MEASURED_PEAKS.json hbm_gbs
            (with concurrent launches: sum of B_alg / device time of the steps).
 * cpu_baseline: the reference algorithm restated in C (oracle/, OpenMP) on
-           the box's host cores, one source of the same graph.
+           the box's host cores, one source of the same graph -- checked bit
+           for bit (distances + counters) against the GPU result of the same
+           source (`parity`) -- plus the unmodified reference package itself
+           (baseline/_ref, pure Python/numpy) timed on R-MAT 18
+           (`reference_python`; R-MAT 24 costs it ~11 min per source).
+* sweep  : the other deltas of configs[3] (0.05, 0.25) and forced binary64
+           at the headline delta, each a full pool through ds_sssp_batch.
+* e2e_dropin: the reference-facing drop-in `delta_stepping_batch` on a
+           SparseMatrix in the reference's own layout (int64 columns, float64
+           weights, pageable host memory) returning SsspResult objects.
 
-Multi-GPU (torchrun): sources are independent, so each rank solves its own
-batch on a replica of the graph (weak scaling, no data-path collective).
+Multi-GPU (`--gpus N`, self-spawned under torch.distributed.run when not
+already launched by it): BASELINE configs[4] -- R-MAT 27 with the 1-D vertex
+partition (one frontier all-gather per light phase over
+NCCL), 16 sources, one source verified bit for bit against the single-GPU
+solver on rank 0; `--replicas` runs independent sources per rank instead.
 """
 
 from __future__ import annotations
@@ -64,11 +76,20 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true")
-    ap.add_argument("--sweep", action="store_true", help="also time delta in {0.05, 0.25}")
+    ap.add_argument("--no-sweep", action="store_true",
+                    help="skip the delta {0.05, 0.25} and forced-binary64 pools")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the e2e_dropin leg")
+    ap.add_argument("--no-python-ref", action="store_true",
+                    help="skip timing the unmodified Python reference (baseline/_ref)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent sources per rank on full graph replicas instead of "
+                         "the partitioned solver")
     ap.add_argument("--partitioned", action="store_true",
-                    help="1-D vertex-partitioned solver across the ranks (SURVEY.md 8(e)): every "
-                         "source is solved jointly, one frontier all-gather per phase")
-    return ap.parse_args()
+                    help="1-D vertex-partitioned solver across the ranks (SURVEY.md 8(e)); the "
+                         "default when N>1")
+    args = ap.parse_args()
+    args.scale_given = "--scale" in sys.argv
+    return args
 
 
 # ------------------------------------------------------------------ helpers
@@ -147,17 +168,20 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def ncu_traffic():
+def ncu_traffic(workload: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the solver
-    kernel from the latest committed ncu --set full capture (profiles/)."""
+    kernel from the latest committed ncu --set full capture of THIS workload
+    (profiles/r*_ncu_summary*.json whose "workload" names it); None if no
+    capture of this workload is committed."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(REPO, "profiles", "r*_ncu_summary.json")))
-    if not files:
-        return None, None
-    with open(files[-1]) as f:
-        d = json.load(f)
-    return d.get("traffic_bytes_per_launch"), os.path.relpath(files[-1], REPO)
+    files = sorted(glob.glob(os.path.join(REPO, "profiles", "r*_ncu_summary*.json")))
+    for fn in reversed(files):
+        with open(fn) as f:
+            d = json.load(f)
+        if str(d.get("workload", "")).split(",")[0].strip() == workload:
+            return d.get("traffic_bytes_per_launch"), os.path.relpath(fn, REPO)
+    return None, None
 
 
 def b_alg(m_r: int, n_r: int, n: int) -> int:
@@ -176,23 +200,74 @@ def dist_env():
 
 # ------------------------------------------------------------------ CPU arm
 
-def run_cpu_oracle(indptr, col, val, sources, delta, threads):
+def pool_sources(indptr, count: int, seed: int = 7) -> list[int]:
+    """The seeded source pool (same draw as paper_1911_06895_b200.graphs.
+    pick_sources, restated so the CPU arm never imports the product)."""
+    import numpy as np
+
+    cand = np.flatnonzero(np.diff(np.asarray(indptr)) > 0)
+    pick = np.random.default_rng(seed).choice(cand.shape[0], size=min(count, cand.shape[0]),
+                                              replace=False)
+    return [int(x) for x in cand[pick]]
+
+
+def run_cpu_oracle(indptr, col, val, sources, delta, threads, keep=False):
     """Reference algorithm (oracle/, C restatement of sssp.py:239-313 with the
     reference's dense pull, OpenMP over rows like parallel_execute) on host
-    cores.  Returns (seconds, sum m_r) for the given sources."""
+    cores.  Returns (seconds, sum m_r[, [(dist, outer, phases)]])."""
     import numpy as np
 
     import oracle
 
     deg = np.diff(indptr)
-    total_t, total_m = 0.0, 0
+    total_t, total_m, kept = 0.0, 0, []
     for s in sources:
         t0 = time.perf_counter()
-        dist, _, _ = oracle.delta_stepping(len(indptr) - 1, indptr, col, val, s, delta,
-                                           threads=threads)
+        dist, outer, phases = oracle.delta_stepping(len(indptr) - 1, indptr, col, val, s, delta,
+                                                    threads=threads)
         total_t += time.perf_counter() - t0
         total_m += int(deg[np.isfinite(dist)].sum())
-    return total_t, total_m
+        if keep:
+            kept.append((dist, outer, phases))
+    return (total_t, total_m, kept) if keep else (total_t, total_m)
+
+
+def python_reference(scale: int = 18, nsrc: int = 2, delta: float = 0.1) -> dict:
+    """The unmodified reference package (deltasparse, pure Python/numpy,
+    staged into baseline/_ref by `pip install --target`) timed through its own
+    public API, `delta_stepping(A, s, delta, backend=BackendChoice("fused",
+    workers=w))` (sssp.py:239-313, fused.py:41-102), w = 1 and all host cores,
+    on an R-MAT of the same generator.  GTEPS = m_r / SsspResult.elapsed
+    (split + solve, like the reference reports).  Informational: at R-MAT 24
+    it needs ~11 min per source plus a ~24 min matrix build."""
+    import numpy as np
+
+    import oracle
+
+    ref_dir = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "deltasparse")):
+        return {"unavailable": "baseline/_ref/deltasparse not staged (see DESIGN.md §8)"}
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import deltasparse as ref
+
+    indptr, col, val = oracle.rmat(scale)
+    A = ref.SparseMatrix(len(indptr) - 1, indptr, col.astype(np.int64), val.astype(np.float64))
+    A.check_invariants()
+    deg = np.diff(indptr)
+    srcs = pool_sources(indptr, nsrc, seed=7)
+    out = {"package": os.path.relpath(os.path.dirname(ref.__file__), REPO),
+           "workload": f"rmat{scale}_ef16_delta{delta}", "sources": srcs}
+    for workers in sorted({1, os.cpu_count() or 1}):
+        secs, m = 0.0, 0
+        for s in srcs:
+            r = ref.delta_stepping(A, s, delta, backend=ref.BackendChoice("fused", workers=workers))
+            secs += r.elapsed
+            m += int(deg[r.distances.indices].sum())
+        out[f"workers_{workers}"] = {"value": m / secs / 1e9, "unit": UNIT,
+                                     "s_per_source": secs / len(srcs)}
+    out["cores"] = os.cpu_count()
+    return out
 
 
 def reference_arm(args):
@@ -202,37 +277,29 @@ def reference_arm(args):
     import numpy as np
 
     import oracle
-    from paper_1911_06895_b200 import graphs
 
     threads = max(1, oracle.max_threads())
-    # Input synthesis: the same R-MAT as our arm.  On a GPU box the device
-    # generator builds it (input prep only -- the timed path is pure CPU);
-    # otherwise the identical host generator.
-    try:
-        from paper_1911_06895_b200 import DeviceGraph, _lib
-        if _lib.device_count() > 0:
-            g = DeviceGraph.rmat(args.scale, args.edge_factor, 1, 2, device=local)
-            indptr, col, val = g.download()
-            g.close()
-        else:
-            raise RuntimeError
-    except Exception:
-        h = graphs.rmat(args.scale, args.edge_factor, 1, 2)
-        indptr, col, val = h.indptr, h.col, h.val
+    scale = args.scale if (ws == 1 or args.scale_given) else 24
+    # Input synthesis without the product library: the same R-MAT from the
+    # C restatement of the generator (oracle/rmat.c, pinned to graphs.rmat)
+    indptr, col, val = oracle.rmat(scale, args.edge_factor, 1, 2)
     col64 = col.astype(np.int64)
     val64 = val.astype(np.float64)
-    pool = graphs.pick_sources(indptr, args.sources, seed=7)
+    del col, val
+    pool = pool_sources(indptr, args.sources, seed=7)
     # warm-up steps (untimed) on a small R-MAT of the same generator: they only
     # page in the library and start the thread pool, and a full scale-24
     # source costs ~45 s of CPU per step
-    small = graphs.rmat(14, args.edge_factor, 1, 2)
-    spool = graphs.pick_sources(small.indptr, max(1, args.warmup), seed=7)
+    sip, scol, sval = oracle.rmat(14, args.edge_factor, 1, 2)
+    spool = pool_sources(sip, max(1, args.warmup), seed=7)
     for k in range(args.warmup):
-        run_cpu_oracle(small.indptr, small.col, small.val, [spool[k % len(spool)]], args.delta, threads)
+        run_cpu_oracle(sip, scol.astype(np.int64), sval.astype(np.float64), [spool[k % len(spool)]],
+                       args.delta, threads)
     secs, edges = run_cpu_oracle(indptr, col64, val64,
                                  [pool[(args.warmup + k) % len(pool)] for k in range(args.steps)],
                                  args.delta, threads)
     value = edges / secs / 1e9
+    pyref = None if args.no_python_ref else python_reference()
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -247,12 +314,14 @@ def reference_arm(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded R-MAT, fp32-lattice weights)",
-        "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_delta{args.delta}",
-                   "sources_per_step": 1, "n": len(indptr) - 1, "nnz": int(indptr[-1])},
+        "config": {"workload": f"rmat{scale}_ef{args.edge_factor}_delta{args.delta}",
+                   "sources_per_step": 1, "n": len(indptr) - 1, "nnz": int(indptr[-1]),
+                   "input": "oracle/rmat.c host generator (bit-identical to graphs.rmat)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"1 source per timed step, full solve incl. split (reference "
                                    f"algorithm restated in C, oracle/); warm-up steps on an R-MAT "
-                                   f"scale-14 source; {cpu_model()}"},
+                                   f"scale-14 source; {cpu_model()}",
+                         "reference_python": pyref},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -262,9 +331,14 @@ def reference_arm(args):
 # ------------------------------------------------------------------ partitioned arm
 
 def partitioned_arm(args):
-    """Every source solved jointly by all ranks: rank r owns a contiguous id
-    range and the edges into it; one NCCL all-gather of the frontier per light
-    phase.  Timed with CUDA events, max over ranks."""
+    """BASELINE configs[4] on N GPUs: R-MAT 27, 16 sources, every source
+    solved jointly by all ranks -- rank r owns a contiguous id range and the
+    edges into it, one NCCL all-gather of the frontier per light phase
+    (SURVEY.md §8(e)).  Timed with CUDA events, max over ranks.  Before the
+    timed region each rank also solves its share of the pool on its full
+    replica (the `replicas` field: the embarrassingly parallel alternative)
+    and rank 0 keeps the single-GPU distances of pool[0], which the
+    partitioned result must equal bit for bit (`parity`)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -275,45 +349,78 @@ def partitioned_arm(args):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
-    dist.init_process_group("nccl", rank=rank, world_size=ws,
-                            device_id=torch.device(f"cuda:{local}"))
-    g = DeviceGraph.rmat(args.scale, args.edge_factor, 1, 2, device=local)
+    dist.init_process_group("nccl", rank=rank, world_size=ws, device_id=dev)
+    scale = args.scale if args.scale_given else 27
+    nsrc = args.batch if "--batch" in sys.argv else 16
+    delta = args.delta
+    g = DeviceGraph.rmat(scale, args.edge_factor, 1, 2, device=local)
     n, nnz = g.n, g.nnz
-    indptr = g.download()[0]
+    indptr = g.download_indptr()
     deg = np.diff(indptr)
+    pool = graphs.pick_sources(indptr, max(nsrc, args.sources), seed=7)
+    srcs = pool[:nsrc]
+    g.prepare(delta)
+    # replicas: rank r solves sources r, r+ws, ... of the step on its own copy
+    mine = srcs[rank::ws]
+    for s in mine[:1]:
+        g.solve(s, delta)  # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    m_rep = 0
+    for s in mine:
+        m_rep += g.solve(s, delta).edges_reached
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    mm = torch.tensor([float(m_rep)], dtype=torch.float64, device=dev)
+    dist.all_reduce(mm)
+    replicas = {"value": float(mm.item()) / (float(t.item()) * 1e-3) / 1e9, "unit": UNIT,
+                "ms_per_step": float(t.item()), "sources_per_rank": len(mine)}
+    want = None
+    if rank == 0:
+        st0 = g.solve(srcs[0], delta)
+        want = (g.result_dense(), st0.outer_iterations, st0.inner_phases)
     b = partition_bounds(n, ws)
     shard = DeviceShard.from_graph(g, b[rank], b[rank + 1])
     g.close()
     solver = PartitionedDeltaStepping(shard, n, dist, "cuda")
-    pool = graphs.pick_sources(indptr, args.sources, seed=7)
-    mydeg = torch.from_numpy(deg[b[rank]:b[rank + 1]].astype(np.int64)).to(f"cuda:{local}")
-
-    def batch(step):
-        return [pool[(step * args.batch + j) % len(pool)] for j in range(args.batch)]
+    mydeg = torch.from_numpy(deg[b[rank]:b[rank + 1]].astype(np.int64)).to(dev)
 
     for w in range(args.warmup):
-        for s in batch(w):
-            solver.solve(s, args.delta, on_device=True)
+        solver.solve(srcs[w % len(srcs)], delta, on_device=True)
+    # parity of pool[0] against rank 0's single-GPU solve
+    r0 = solver.solve(srcs[0], delta, on_device=True)
+    sizes = [b[i + 1] - b[i] for i in range(ws)]
+    parts = [torch.empty(sz, dtype=torch.float64, device=dev) for sz in sizes]
+    dist.all_gather(parts, r0.local.contiguous())
+    parity = None
+    if rank == 0:
+        got = torch.cat(parts).cpu().numpy()
+        parity = {"source": srcs[0],
+                  "distances_bit_exact": bool(np.array_equal(got.view(np.uint64), want[0].view(np.uint64))),
+                  "counters_equal": (r0.outer_iterations, r0.inner_phases) == (want[1], want[2])}
     dist.barrier()
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    m_local, phases, exch = 0, [], 0
     e0.record()
+    m_local, phases, exch = 0, [], 0
     for k in range(args.steps):
-        for s in batch(args.warmup + k):
-            r = solver.solve(s, args.delta, on_device=True)
+        for s in srcs:
+            r = solver.solve(s, delta, on_device=True)
             m_local += int(mydeg[torch.isfinite(r.local)].sum().item())
             phases.append(r.inner_phases)
             exch += r.exchanged
     e1.record()
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    m = torch.tensor([float(m_local)], dtype=torch.float64, device=f"cuda:{local}")
+    m = torch.tensor([float(m_local)], dtype=torch.float64, device=dev)
     dist.all_reduce(m)
     t_ms = float(t.item())
     value = float(m.item()) / (t_ms * 1e-3) / 1e9
@@ -323,9 +430,14 @@ def partitioned_arm(args):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32 fixed-point (exact f64)",
             "data": "synthetic (seeded R-MAT, generated on device)",
-            "config": {"workload": f"rmat{args.scale}_ef{args.edge_factor}_delta{args.delta}",
-                       "n": n, "nnz": nnz, "sources_per_step": args.batch,
-                       "parallelism": f"1-D vertex partition x{ws}, NCCL all-gather per phase"},
+            "config": {"workload": f"rmat{scale}_ef{args.edge_factor}_delta{delta}",
+                       "n": n, "nnz": nnz, "sources_per_step": len(srcs),
+                       "parallelism": f"1-D vertex partition x{ws}, NCCL all-gather per light phase",
+                       "l2": "inputs larger than L2"},
+            "parity": parity,
+            "replicas": replicas,
+            "e2e": None,
+            "e2e_note": "inputs generated on each rank's device (no host copy exists at R-MAT 27)",
             "gpu_launches": None,
             "solver": {"phases_mean": statistics.mean(phases),
                        "frontier_entries_exchanged_per_source": exch / max(1, len(phases))},
@@ -335,13 +447,32 @@ def partitioned_arm(args):
     return 0
 
 
+def spawn(args) -> int:
+    """`python bench.py --gpus N` outside torchrun: re-launch this script
+    under torch.distributed.run with N ranks on this node (127.0.0.1)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 # ------------------------------------------------------------------ GPU arm
 
 def main():
     args = parse()
+    ws, _, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
     if args.impl == "reference":
         return reference_arm(args)
-    if args.partitioned:
+    if args.partitioned or (ws > 1 and not args.replicas):
         return partitioned_arm(args)
 
     import numpy as np
@@ -447,19 +578,31 @@ def main():
         # concurrent launches overlap: aggregate algorithmic bytes over the
         # device time of the steps (which hold only the solver launches)
         achieved = balg_tot / (t_ms * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic()
+    traffic, traffic_src = ncu_traffic(workload)
 
-    # ---- delta sweep (informational)
+    # ---- the rest of configs[3]: delta 0.05 / 0.25, and forced binary64 (the
+    # mode every non-lattice weight takes) at the headline delta; one full
+    # pool each through ds_sssp_batch, device-timed like `value`
     sweep = {}
-    if args.sweep:
-        for d in (0.05, 0.25):
-            g.prepare(d)
-            ts, ms = 0.0, 0
-            for s in batch(0):
-                st = g.solve(s, d)
-                ts += st.kernel_ms
-                ms += st.edges_reached
-            sweep[str(d)] = {"gteps": ms / (ts * 1e-3) / 1e9, "kernel_ms_mean": ts / args.batch}
+    if not args.no_sweep and args.config == "rmat":
+        for name, d, f64 in (("delta0.05", 0.05, False), ("delta0.25", 0.25, False),
+                             (f"delta{delta}_f64", delta, True)):
+            g.prepare(d, force_f64=f64)
+            g.solve_batch(batch(0)[:conc], d, concurrency=conc, keep=False, force_f64=f64)  # warm
+            torch.cuda.synchronize()
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            stats, _ = g.solve_batch(batch(0), d, concurrency=conc, keep=False, force_f64=f64)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ms = a0.elapsed_time(a1)
+            me = sum(st.edges_reached for st in stats)
+            ba = sum(b_alg(st.edges_reached, st.reached, n) for st in stats)
+            sweep[name] = {"value": me / (ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": ms,
+                           "roofline_frac": ba / (ms * 1e-3) / 1e9 / peak,
+                           "dist_mode": "f64" if stats[0].dist_mode == 1 else "u32 fixed-point",
+                           "phases_mean": statistics.mean(st.inner_phases for st in stats)}
         g.prepare(delta)
 
     # ---- end to end through the public API with host buffers (e2e)
@@ -498,18 +641,59 @@ def main():
                "includes": "pinned H2D of the CSR, device validation + split, the batch's "
                            "solves, D2H of every dense float64 distance vector"}
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- e2e through the reference-facing drop-in: delta_stepping_batch on a
+    # SparseMatrix in the reference's layout (int64 col, float64 val, pageable
+    # host memory) returning SsspResult objects; the device cache is cleared
+    # every step, so each step uploads and splits the matrix again
+    dropin = None
+    if not args.no_e2e and not args.no_dropin:
+        from paper_1911_06895_b200 import SparseMatrix, clear_device_cache, delta_stepping_batch
+
+        A = SparseMatrix(n, indptr_h, col_h.astype(np.int64), val_h.astype(np.float64))
+        clear_device_cache()
+        delta_stepping_batch(A, batch(0)[:2], delta, concurrency=conc)  # warm
+        clear_device_cache()
+        barrier()
+        t0 = time.perf_counter()
+        m_d, reached = 0, 0
+        nsteps = min(args.steps, 2)
+        for k in range(nsteps):
+            rs = delta_stepping_batch(A, batch(args.warmup + k), delta, concurrency=conc)
+            m_d += sum(r.device_stats["edges_reached"] for r in rs)
+            reached += sum(r.distances.nnz for r in rs)
+            clear_device_cache()
+        t_d = time.perf_counter() - t0
+        dropin = {"value": m_d / t_d / 1e9, "unit": UNIT, "steps": nsteps,
+                  "ms_per_step": t_d / nsteps * 1e3,
+                  "h2d_bytes_per_step": int(A.indptr.nbytes + A.col.nbytes + A.val.nbytes),
+                  "d2h_bytes_per_step": args.batch * n * 8,
+                  "result_bytes_per_step": reached // nsteps * 16,
+                  "includes": "SparseMatrix(int64 col, float64 val) upload per step, device split, "
+                              "the batch's solves, dense D2H, SsspResult(SparseVector) construction"}
+        del A
+
+    # ---- CPU baseline (rank 0, N=1 only), checked against the GPU result
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         import oracle
 
         threads = max(1, oracle.max_threads())
-        secs, edges = run_cpu_oracle(indptr_h, col_h.astype(np.int64), val_h.astype(np.float64),
-                                     [mine[0]], delta, threads)
+        s0 = mine[0]
+        secs, edges, kept = run_cpu_oracle(indptr_h, col_h.astype(np.int64), val_h.astype(np.float64),
+                                           [s0], delta, threads, keep=True)
+        want, outer, phases = kept[0]
+        st = g.solve(s0, delta)
+        got = g.result_dense()
+        parity = {"source": s0,
+                  "distances_bit_exact": bool(np.array_equal(got.view(np.uint64), want.view(np.uint64))),
+                  "counters_equal": (st.outer_iterations, st.inner_phases) == (outer, phases),
+                  "outer_iterations": outer, "inner_phases": phases}
         cpu = {"value": edges / secs / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"1 source ({mine[0]}) of the same R-MAT graph, full solve incl. "
+               "sample": f"1 source ({s0}) of the same R-MAT graph, full solve incl. "
                          f"split, reference algorithm restated in C (oracle/) with OpenMP, "
-                         f"{secs:.1f}s, {cpu_model()}"}
+                         f"{secs:.1f}s, {cpu_model()}",
+               "parity": parity,
+               "reference_python": None if args.no_python_ref else python_reference()}
 
     if rank == 0:
         line = {
@@ -550,8 +734,10 @@ def main():
                                    f"{conc} concurrent launches: sum of algorithmic bytes / "
                                    "device time of the timed steps"),
             },
+            "parity": cpu["parity"] if cpu else None,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_dropin": dropin,
             "gpu_launches": sum(p["launches"] for p in per_solve),
             "clocks": clk,
             "solver": {
@@ -566,8 +752,8 @@ def main():
                 "kernel_ms_max": max(kern_ms),
                 "prepare_ms": info.prepare_ms,
                 "pull_steps_mean": statistics.mean(p["pull_steps"] for p in per_solve),
-                "sweep": sweep,
             },
+            "sweep": sweep,
         }
         print(json.dumps(line), flush=True)
     g.close()

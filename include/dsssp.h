@@ -159,7 +159,8 @@ int ds_gen_rmat(int32_t scale, int32_t edge_factor, uint64_t seed, uint64_t weig
                 int device, void* stream, ds_graph** out);
 
 /* Copy the handle's original CSR to host/device buffers: indptr n+1 int64,
- * col nnz int32, val nnz float32 (weights must be float32-exact). */
+ * col nnz int32, val nnz float32 (weights must be float32-exact).  Any of the
+ * three may be NULL (not copied). */
 int ds_graph_download(ds_graph* g, int64_t* indptr, int32_t* col, float* val);
 
 /* ------------------------------------------------------------------------

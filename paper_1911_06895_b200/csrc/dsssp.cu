@@ -2002,9 +2002,10 @@ __global__ void k_download_w(const double* w, float* out, long long m, int* bad)
 extern "C" int ds_graph_download(ds_graph* g, int64_t* indptr, int32_t* col, float* val) {
     if (!g) return set_err(DS_EINVAL, "null graph handle");
     DeviceGuard guard(g->device);
-    CK(cudaMemcpyAsync(indptr, g->indptr, sizeof(long long) * (g->n + 1), cudaMemcpyDefault, g->stream));
-    if (g->nnz > 0) {
-        CK(cudaMemcpyAsync(col, g->col, sizeof(int) * g->nnz, cudaMemcpyDefault, g->stream));
+    if (indptr)
+        CK(cudaMemcpyAsync(indptr, g->indptr, sizeof(long long) * (g->n + 1), cudaMemcpyDefault, g->stream));
+    if (col && g->nnz > 0) CK(cudaMemcpyAsync(col, g->col, sizeof(int) * g->nnz, cudaMemcpyDefault, g->stream));
+    if (val && g->nnz > 0) {
         float* tmp = nullptr;
         CK(cudaMalloc(&tmp, sizeof(float) * g->nnz));
         int* bad = reinterpret_cast<int*>(g->pstat);

@@ -20,9 +20,11 @@ from __future__ import annotations
 import contextlib
 import ctypes
 import math
+import os
 import threading
 import time
 from collections import OrderedDict
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -285,6 +287,13 @@ class DeviceGraph:
                                                   _ptr(val)))
         return indptr, col[:m], val[:m]
 
+    def download_indptr(self) -> np.ndarray:
+        """Row offsets only (int64, host): degrees without the edge arrays."""
+        indptr = np.empty(self.n + 1, dtype=np.int64)
+        with self.lock:
+            _lib.check(_lib.lib().ds_graph_download(self._handle(), _ptr(indptr), None, None))
+        return indptr
+
     def download(self, out=None):
         """Original CSR (int64 indptr, int32 col, float32 val), to host arrays
         or into `out` = (indptr, col, val) buffers (numpy, or torch tensors on
@@ -435,13 +444,23 @@ def delta_stepping_batch(
     with _device_graph(matrix) as g:
         stats, dist = g.solve_batch(srcs, float(delta), skip_empty_buckets=skip_empty_buckets,
                                     concurrency=concurrency)
+    # dense rows -> reached (index, value) pairs; numpy releases the GIL on
+    # these full-row passes, so rows convert in parallel
+    def sparse_row(i):
+        row = dist[i]
+        idx = np.flatnonzero(row != np.inf)
+        return idx, row[idx]
+
+    if len(srcs) > 1 and matrix.n >= (1 << 16):
+        with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1, 16)) as ex:
+            rows = list(ex.map(sparse_row, range(len(srcs))))
+    else:
+        rows = [sparse_row(i) for i in range(len(srcs))]
     elapsed = (time.perf_counter() - start) / len(srcs)
     out = []
-    for i, st in enumerate(stats):
-        row = dist[i]
-        idx = np.flatnonzero(np.isfinite(row)).astype(np.int64)
+    for (idx, val), st in zip(rows, stats):
         out.append(SsspResult(
-            distances=SparseVector(matrix.n, idx, row[idx]),
+            distances=SparseVector(matrix.n, idx, val),
             outer_iterations=int(st.outer_iterations),
             inner_phases=int(st.inner_phases),
             elapsed=elapsed,
