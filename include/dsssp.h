@@ -58,6 +58,7 @@ extern "C" {
 /* ds_sssp flags */
 #define DS_FLAG_SKIP_EMPTY 1u /* outer_iterations counts like skip_empty_buckets=True */
 #define DS_FLAG_FORCE_F64 2u  /* disable the exact 32-bit fixed-point distance mode */
+#define DS_FLAG_NO_LEX 4u     /* keep the reference's bucket schedule (no sub-buckets) */
 
 /* distance modes reported in ds_prep_info / ds_stats */
 #define DS_MODE_FIXED32 0 /* d * 2^frac_bits held exactly in uint32 */

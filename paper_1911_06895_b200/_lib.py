@@ -17,7 +17,7 @@ DS_EPARSE, DS_EVALID = 6, 7
 DS_FMT_MTX, DS_FMT_EDGES = 0, 1
 DS_IDX_I32, DS_IDX_I64 = 0, 1
 DS_W_F32, DS_W_F64, DS_W_I32 = 0, 1, 2
-DS_FLAG_SKIP_EMPTY, DS_FLAG_FORCE_F64 = 1, 2
+DS_FLAG_SKIP_EMPTY, DS_FLAG_FORCE_F64, DS_FLAG_NO_LEX = 1, 2, 4
 DS_MODE_FIXED32, DS_MODE_F64 = 0, 1
 
 # Every entry point include/dsssp.h declares (checked by the CPU tests).

@@ -45,6 +45,9 @@
 #include <cub/block/block_scan.cuh>
 #include <math_constants.h>
 
+#include <climits>
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ds {
@@ -128,6 +131,47 @@ struct ModeF64 {
         return __dadd_rn(lo, __longlong_as_double((long long)minW)) >= hi;
     }
 };
+
+// ---------------------------------------------------------------- lex mode
+//
+// The reference's counters (outer_iterations, inner_phases) follow its
+// Jacobi light phases inside each bucket [i*delta, (i+1)*delta) -- a schedule
+// that re-pushes a vertex's light row every time it improves (R-MAT 24:
+// 6x nnz(A_L)).  Lex mode computes the same distances with ksub finer internal
+// buckets per reference bucket (fewer re-pushes) and recovers the counters
+// exactly from hop counts carried in the distance word:
+//   key = (D << kHopBits) | h,   min over keys = min D, then min h.
+// A push u -> v with weight W carries h_u + 1 when the edge is a reference-
+// light edge (W <= WD) landing in u's reference bucket (D_u + W < HD), else 0
+// (the value is part of a later bucket's starting state).  Integer adds are
+// exact, so the lexicographic minimum over walks is schedule-independent and
+// h(v) is the fewest light hops over the walks achieving D(v) inside the
+// bucket, counted from the bucket's starting values.  The reference's k-th
+// phase of bucket i is non-empty iff some vertex of the bucket has h >= k
+// (Jacobi round k finds exactly the <= k-hop walks), so the bucket runs
+// 1 + max h phases; a bucket is visited iff some final value lies in it.
+// Keys need D < 2^(32 - kHopBits) - 1 and h < 2^kHopBits: a larger sum or
+// hop count raises the overflow flag and the solve reruns in binary64 mode.
+constexpr int kHopBits = 6;
+constexpr unsigned kHopMask = (1u << kHopBits) - 1;
+constexpr unsigned long long kLexDLimit = (1ull << (32 - kHopBits)) - 1;
+
+template <class M>
+struct KParams;
+
+// push candidate: plain add, or the lex key (fixed point, p.lex)
+template <bool LEX, class M>
+__device__ __forceinline__ bool padd(const KParams<M>& p, typename M::D ku, const typename M::Edge& e,
+                                     typename M::D hd, typename M::D& nd) {
+    if constexpr (LEX && std::is_same<M, ModeFixed>::value) {
+        // 32-bit: D < 2^26 and every weight W < 2^26 (checked at prepare)
+        const unsigned s = (ku >> kHopBits) + e.y;
+        const unsigned h = (e.y <= p.WD && s < hd) ? (ku & kHopMask) + 1u : 0u;
+        nd = (s << kHopBits) | h;
+        return s < (unsigned)kLexDLimit && h <= kHopMask;
+    }
+    return M::add(ku, e, nd);
+}
 
 // ---------------------------------------------------------------- control block
 
@@ -214,7 +258,7 @@ struct StepSlot {
     unsigned long long next_min;      // capture (range mode): min D >= H
     unsigned long long append_count;  // relax / pull (light): next-frontier size
     unsigned int flags;               // bit0: fixed-point overflow
-    unsigned int pad;
+    unsigned int hopmax;              // lex mode: largest hop count of a captured S
     unsigned long long pad2[3];
 };
 
@@ -285,6 +329,12 @@ struct KParams {
     unsigned long long hpull_min;
     unsigned long long nH;
     unsigned long long min_heavy;  // smallest heavy weight: fixed W, or f64 bits
+    // Sub-bucketed solve with lexicographic keys (fixed point only; see
+    // "lex mode" below): ksub internal buckets per reference bucket, dist
+    // words hold (D << kHopBits) | hops, WD = largest reference-light W.
+    int lex;
+    int ksub_log2;  // ksub = 1 << ksub_log2 (shifts, no 64-bit divisions)
+    unsigned WD;
     const long long* indptr;  // original CSR row offsets (for m_r)
     const long long* Lptr;
     const Edge* Ledges;
@@ -336,12 +386,24 @@ __device__ __forceinline__ D* queue_vals(WarpSmem<D>& ws) {
 #endif
 }
 
+// lex-mode accounting of the reference buckets (kept by thread 0 of every
+// CTA in shared memory: the values are uniform, and registers are scarce in
+// the persistent kernel)
+struct LexAcc {
+    long long cur_ref;  // reference bucket being accumulated
+    unsigned long long phases, visited;
+    unsigned hop_acc;
+    int any;
+    int over;  // the reference's phase count exceeded the ceiling
+};
+
 template <class D>
 struct Smem {
     WarpSmem<D> w[kWarps];
     unsigned long long red[kWarps];
     unsigned long long red2[kWarps];
     int ok;
+    LexAcc lx;
 };
 
 // ---------------------------------------------------------------- warp / block utils
@@ -783,6 +845,19 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
             deg[j] = in[j] ? __ldg(ptr + vtx[j] + 1) - off[j] : 0;
             if (in[j] && clear_bits) clear_bits[(unsigned)vtx[j] >> 5] = 0u;
         }
+        if (!APPEND_S && !VALS && std::is_same<M, ModeFixed>::value) {
+            // lex mode, S capture of an internal bucket: its largest hop count
+            // (S holds the bucket's final keys)
+            if (p.lex) {
+                unsigned hm = 0;
+#pragma unroll
+                for (int j = 0; j < kListPer; ++j)
+                    if (in[j]) hm = max(hm, (unsigned)dv[j] & kHopMask);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+                if (lane == 0 && hm) atomicMax(&slot->hopmax, hm);
+            }
+        }
         if (APPEND_S) {
             bool news[kListPer];
 #pragma unroll
@@ -827,11 +902,11 @@ __device__ __forceinline__ void csum_lower(const KParams<M>& p, unsigned v, type
 // pulled form of the heavy relaxation, r = A_H^T (t o S) (sssp.py:206-227),
 // restricted to the rows it can still lower.  See the direction choice at
 // POS_HEAVY for why this is exact.
-template <class M, bool LIGHT, bool LOCALW = false, bool SUM = false, bool PULL = false>
+template <class M, bool LIGHT, bool LOCALW = false, bool SUM = false, bool PULL = false, bool LEX = false>
 __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                            unsigned long long E, unsigned long long Rc,
                            const typename M::Edge* edges, typename M::D H, int* out_list,
-                           unsigned* fbits) {
+                           unsigned* fbits, typename M::D HD = 0) {
     using D = typename M::D;
     using Edge = typename M::Edge;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1018,7 +1093,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             for (int j = 0; j < kRelPer; ++j) {
                 if (32 * j < left && du[j] < H) {
                     D nd;
-                    if (!M::add(du[j], ed[j], nd)) {
+                    if (!padd<LEX>(p, du[j], ed[j], HD, nd)) {
                         overflow = true;
                     } else if (nd < cur[j]) {
                         const unsigned v = (unsigned)DS_DU(j);
@@ -1037,7 +1112,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             cur[j] = (D)0;
             nd[j] = (D)0;  // defined on every path (see ed[] above)
             if (32 * j < left) {
-                if (M::add(DS_DU(j), ed[j], nd[j])) {
+                if (padd<LEX>(p, DS_DU(j), ed[j], HD, nd[j])) {
                     // a stale (L1) value is >= the current one: it can only
                     // cause a redundant atomic, never a missed improvement
                     const unsigned v = M::col(ed[j]);
@@ -1292,7 +1367,35 @@ __device__ void commit_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSl
 
 // ---------------------------------------------------------------- the solver
 
-template <class M, bool SMALL>
+// Window of internal bucket idx: keys [L, H) and the reference bucket's upper
+// bound HD in distance units.  Classic: idx is the reference bucket (keys =
+// distances).  Lex: reference bucket idx / ksub split into ksub integer
+// sub-windows, shifted into key space.
+template <class M>
+__device__ __forceinline__ void lex_window(const KParams<M>& p, bool lex, long long idx, double& lo,
+                                           double& hi, typename M::D& L, typename M::D& H,
+                                           typename M::D& HD) {
+    using D = typename M::D;
+    const int kl = lex ? p.ksub_log2 : 0;
+    const long long ridx = idx >> kl;
+    lo = (double)ridx * p.delta;
+    hi = (double)(ridx + 1) * p.delta;
+    D LD;
+    M::window(lo, hi, p.frac, LD, HD);
+    if (!lex) {
+        L = LD;
+        H = HD;
+        return;
+    }
+    const unsigned long long w = (unsigned long long)HD - LD;
+    const unsigned long long t = (unsigned long long)idx & ((1ull << kl) - 1);
+    const unsigned long long a = LD + ((t * w) >> kl);
+    const unsigned long long b = t + 1 == (1ull << kl) ? (unsigned long long)HD : LD + (((t + 1) * w) >> kl);
+    L = (D)min(a << kHopBits, (unsigned long long)M::INF);
+    H = (D)min(b << kHopBits, (unsigned long long)M::INF);
+}
+
+template <class M, bool SMALL, bool LEX = false>
 __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     sssp_persistent_kernel(const KParams<M> p) {
     using D = typename M::D;
@@ -1335,6 +1438,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 StepSlot* s = &c->slot[k];
                 s->re_packed = s->front_count = s->append_count = 0;
                 s->flags = 0;
+                s->hopmax = 0;
                 s->next_min = ~0ull;
             }
             c->s_count[0] = c->s_count[1] = 0;
@@ -1377,6 +1481,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             StepSlot* s = &c->slot[(st + 1) % 3];
             s->re_packed = s->front_count = s->append_count = 0;
             s->flags = 0;
+            s->hopmax = 0;
             s->next_min = ~0ull;
         }
         const bool ok = grid_sync(c, gen, deadline, sm);
@@ -1413,6 +1518,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             StepSlot* x = &c->xslot;
             x->re_packed = x->front_count = x->append_count = 0;
             x->flags = 0;
+            x->hopmax = 0;
             x->next_min = ~0ull;
         }
     };
@@ -1422,11 +1528,53 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         p.pull_enabled ? (unsigned long long)(p.pull_heavy * (float)p.Hpull.nnz) : ~0ull;
     unsigned long long nf = 0;
 
+    // lex mode (fixed point, non-SMALL kernel, p.lex): idx counts internal
+    // buckets, ksub per reference bucket; the reference's counters are
+    // accumulated per reference bucket in sm.lx by thread 0
+    constexpr bool kLex = LEX && std::is_same<M, ModeFixed>::value && !SMALL;
+    static_assert(!LEX || kLex, "lex mode: fixed point, non-SMALL kernel only");
+    if (kLex && threadIdx.x == 0) {
+        sm.lx.cur_ref = -1;
+        sm.lx.phases = sm.lx.visited = 0;
+        sm.lx.hop_acc = 0;
+        sm.lx.any = sm.lx.over = 0;
+    }
+    // close the reference bucket (thread 0): it ran 1 + max h phases
+    auto ref_flush = [&]() {
+        if (sm.lx.any) {
+            sm.lx.phases += 1ull + sm.lx.hop_acc;
+            ++sm.lx.visited;
+            if ((long long)sm.lx.phases > p.ceiling) sm.lx.over = 1;
+        }
+        sm.lx.any = 0;
+        sm.lx.hop_acc = 0;
+    };
+
     for (;;) {
-        const double lo = (double)idx * p.delta;
-        const double hi = (double)(idx + 1) * p.delta;
-        D L, H;
-        M::window(lo, hi, p.frac, L, H);
+        D L, H, HD;
+        double lo, hi;  // the reference bucket's bounds (f64)
+        lex_window<M>(p, kLex, idx, lo, hi, L, H, HD);
+        if (kLex) {
+            D LD, HD2;
+            M::window(lo, hi, p.frac, LD, HD2);
+            if ((unsigned long long)HD - LD > (unsigned long long)p.WD + 1ull) {
+                // a reference-heavy edge could land inside its own bucket (a
+                // rounding corner of fl(i*delta)): leave to the exact f64 mode
+                status = kDevOverflow;
+                break;
+            }
+            const long long ridx = idx >> p.ksub_log2;
+            __syncthreads();
+            if (threadIdx.x == 0 && ridx != sm.lx.cur_ref) {
+                ref_flush();
+                sm.lx.cur_ref = ridx;
+            }
+            __syncthreads();
+            if (sm.lx.over) {
+                status = 2;  // DS_ENOCONVERGE: the reference's phase count
+                break;
+            }
+        }
 
         if (pos == POS_BUCKET) {
             // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
@@ -1440,17 +1588,33 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             if (fc == 0) {
                 const unsigned long long nm = ldcg(&prev()->next_min);
                 if (nm == ~0ull) break;  // nothing stored beyond: done
-                idx = bucket_index_of(M::to_f64((D)nm, p.frac), p.delta);
+                if (kLex) {
+                    // next internal bucket: the reference bucket of the value,
+                    // then the sub-window holding it
+                    const int kl = p.ksub_log2;
+                    const D dn = (D)nm >> kHopBits;
+                    const long long rn = bucket_index_of(M::to_f64(dn, p.frac), p.delta);
+                    D a, b;
+                    M::window((double)rn * p.delta, (double)(rn + 1) * p.delta, p.frac, a, b);
+                    const unsigned long long w = (unsigned long long)b - a;
+                    long long t = (1ll << kl) - 1;
+                    while (t > 0 && (unsigned long long)dn < a + (((unsigned long long)t * w) >> kl)) --t;
+                    idx = (rn << kl) + t;
+                } else {
+                    idx = bucket_index_of(M::to_f64((D)nm, p.frac), p.delta);
+                }
                 continue;
             }
             ++visited;
+            if (kLex && threadIdx.x == 0) sm.lx.any = 1;
             pos = POS_PHASE;
         }
 
         if (pos == POS_PHASE) {
             // ---- one light phase (sssp.py:292-301)
             ++phases;
-            if ((long long)phases > p.ceiling) {
+            if ((long long)phases > ((kLex) ? (p.ceiling > LLONG_MAX / 64 ? LLONG_MAX : p.ceiling * 64)
+                                                         : p.ceiling)) {
                 status = 2;  // DS_ENOCONVERGE
                 break;
             }
@@ -1473,6 +1637,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                         if (threadIdx.x == 0) {
                             a->re_packed = a->front_count = a->append_count = 0;
                             a->flags = 0;
+                            a->hopmax = 0;
                         }
                         __syncthreads();
                         const unsigned long long lE = lre & kMask33;
@@ -1495,6 +1660,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                         if (threadIdx.x == 0) {
                             b->re_packed = b->front_count = b->append_count = 0;
                             b->flags = 0;
+                            b->hopmax = 0;
                         }
                         __syncthreads();
                         capture_list<M, true, false, true>(p, sm, b, p.F[lpp], nullptr, lnf, p.Lptr,
@@ -1560,8 +1726,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 continue;
             } else if (E > 0) {
                 escanned += E;
-                relax_step<M, true, false, kSum>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Ledges, H,
-                                    p.F[pp], p.fbits[phases & 1]);
+                relax_step<M, true, false, kSum, false, kLex>(p, sm, &c->slot[st % 3], E, re >> kPackShift,
+                                                             p.Ledges, H, p.F[pp], p.fbits[phases & 1], HD);
                 if (!end_step(1, E)) return;
                 if (ldcg(&prev()->flags) & 1u) {
                     status = kDevOverflow;
@@ -1606,6 +1772,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                     if (threadIdx.x == 0) {
                         a->re_packed = a->front_count = a->append_count = 0;
                         a->flags = 0;
+                        a->hopmax = 0;
                     }
                     __syncthreads();
                     capture_list<M, false, false, true>(p, sm, a, p.S[bpar], nullptr, scount, p.Hptr,
@@ -1637,6 +1804,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                                               p.Hptr, nullptr, nullptr, nullptr);
                 if (!end_step(3, scount)) return;
                 re = ldcg(&prev()->re_packed);
+                if (kLex && threadIdx.x == 0)
+                    sm.lx.hop_acc = max(sm.lx.hop_acc, ldcg(&prev()->hopmax));
             }
             const unsigned long long E = heavy_done ? 0ull : (re & kMask33);
             hset += re & kMask33;  // S's rows are settled: their heavy edges leave the pull volume
@@ -1653,8 +1822,13 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             //  * rows >= H are the only possible targets; min is order-free.
             if (!heavy_done && E > 0 && p.hpull && E >= p.hpull_min) {
                 const unsigned long long U = p.nH > hset ? p.nH - hset : 0ull;
+                D Lw = L, Hw = H;  // the internal window in distance units
+                if (kLex) {
+                    Lw = L >> kHopBits;
+                    Hw = H == M::INF ? (D)kLexDLimit : (D)(H >> kHopBits);
+                }
                 if ((double)E > (double)p.hpull_ratio * (double)U &&
-                    M::heavy_beyond(L, H, lo, hi, p.min_heavy)) {
+                    M::heavy_beyond(Lw, Hw, lo, hi, p.min_heavy)) {
                     capture_range<M, false, true>(p, sm, &c->slot[st % 3], H, M::INF, nullptr, nullptr,
                                                   (unsigned long long)n_scan, nullptr, 0ull, p.Hptr);
                     if (!end_step(11, (unsigned long long)n_scan)) return;
@@ -1663,8 +1837,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                     ++npull;
                     if (Ep > 0) {
                         escanned += Ep;
-                        relax_step<M, false, false, kSum, true>(p, sm, &c->slot[st % 3], Ep, pre >> kPackShift,
-                                                                p.Hedges, H, nullptr, nullptr);
+                        relax_step<M, false, false, kSum, true, kLex>(p, sm, &c->slot[st % 3], Ep, pre >> kPackShift,
+                                                                p.Hedges, H, nullptr, nullptr, HD);
                         if (!end_step(12, Ep)) return;
                         if (ldcg(&prev()->flags) & 1u) {
                             status = kDevOverflow;
@@ -1693,8 +1867,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 }
             } else if (E > 0) {
                 escanned += E;
-                relax_step<M, false, false, kSum>(p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Hedges, H,
-                                     nullptr, nullptr);
+                relax_step<M, false, false, kSum, false, kLex>(p, sm, &c->slot[st % 3], E, re >> kPackShift,
+                                                              p.Hedges, H, nullptr, nullptr, HD);
                 if (!end_step(4, E)) return;
                 if (ldcg(&prev()->flags) & 1u) {
                     status = kDevOverflow;
@@ -1718,6 +1892,14 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         }
     }
 
+    if (kLex) {
+        __syncthreads();
+        if (threadIdx.x == 0 && !status) ref_flush();
+        __syncthreads();
+        if (!status && sm.lx.over) status = 2;  // DS_ENOCONVERGE: the reference's count
+        phases = sm.lx.phases;
+        visited = sm.lx.visited;
+    }
     if (status) {
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             c->status = status;
@@ -1755,7 +1937,10 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             }
             D d[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) d[j] = sv[j] < n_scan ? __ldcg(p.dist + sv[j]) : M::INF;
+            for (int j = 0; j < 8; ++j) {
+                d[j] = sv[j] < n_scan ? __ldcg(p.dist + sv[j]) : M::INF;
+                if (kLex && d[j] != M::INF) d[j] >>= kHopBits;  // key -> distance
+            }
             double o[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {

@@ -1,0 +1,100 @@
+"""Lex mode (sssp_kernel.cuh "lex mode"): the solver runs ksub internal
+buckets per reference bucket and recovers the reference's counters from hop
+counts carried in the distance keys.  On by default only for large graphs,
+so here it is forced (DS_LEX_K) on small ones and checked bit for bit --
+distances, outer_iterations in both skip modes, inner_phases -- against the
+golden vectors recorded from the reference and against the oracle."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import criterion1_graphs, graph_from_json, vec_hash
+from paper_1911_06895_b200 import (
+    DeviceGraph,
+    SparseMatrix,
+    clear_device_cache,
+    delta_stepping,
+    graphs,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+@pytest.fixture(params=[2, 4, 8])
+def lex_k(request, monkeypatch):
+    monkeypatch.setenv("DS_LEX_K", str(request.param))
+    clear_device_cache()
+    yield request.param
+    clear_device_cache()
+
+
+def _check(a, s, d):
+    r = delta_stepping(a, s, d)
+    want, outer, phases = oracle.delta_stepping(a.n, a.indptr, a.col, a.val, s, d, threads=4)
+    idx = np.flatnonzero(np.isfinite(want))
+    assert np.array_equal(r.distances.indices, idx), (s, d)
+    assert np.array_equal(_bits(r.distances.values), _bits(want[idx])), (s, d)
+    assert (r.outer_iterations, r.inner_phases) == (outer, phases), (s, d)
+    rs = delta_stepping(a, s, d, skip_empty_buckets=True)
+    _, outer_s, phases_s = oracle.delta_stepping(a.n, a.indptr, a.col, a.val, s, d,
+                                                 skip_empty_buckets=True, threads=4)
+    assert rs.distances == r.distances
+    assert (rs.outer_iterations, rs.inner_phases) == (outer_s, phases_s), (s, d)
+    return r
+
+
+def test_lex_rmat_deltas(lex_k):
+    a = graphs.rmat(15, seed=3, weight_seed=4)
+    for d in (0.05, 0.1, 0.25, 0.7):
+        for s in graphs.pick_sources(a.indptr, 3, seed=17):
+            r = _check(a, int(s), d)
+            assert r.device_stats["dist_mode"] == 0  # fixed point (lex needs it)
+
+
+def test_lex_er_integer_weights(lex_k):
+    a = graphs.erdos_renyi(1024, seed=0)  # directed: heavy steps push
+    for d in (3.0, 5.0, 10.0):
+        for s in (0, 17, 900):
+            _check(a, s, d)
+
+
+def test_lex_golden_corpus(lex_k, golden):
+    # the reference's own criterion-1 corpus (float 10(1-U), int, unit
+    # weights) at its recorded deltas: the golden hashes and counters
+    for (a, s, kind), rec in list(zip(criterion1_graphs(), golden["criterion1"]))[::7]:
+        for run in rec["runs"]:
+            d = float.fromhex(run["delta"])
+            r = delta_stepping(a, s, d)
+            assert vec_hash(r.distances.indices, r.distances.values) == run["hash"]
+            assert (r.outer_iterations, r.inner_phases) == (run["outer"], run["phases"])
+            rs = delta_stepping(a, s, d, skip_empty_buckets=True)
+            assert (rs.outer_iterations, rs.inner_phases) == (run["outer_skip"], run["phases_skip"])
+    for rec in golden["odd_delta"]:
+        n, indptr, col, val = graph_from_json(rec["graph"])
+        a = SparseMatrix(n, indptr, col, val)
+        for run in rec["runs"]:
+            d = float.fromhex(run["delta"])
+            r = delta_stepping(a, rec["source"], d)
+            assert vec_hash(r.distances.indices, r.distances.values) == run["hash"]
+            assert (r.outer_iterations, r.inner_phases) == (run["outer"], run["phases"])
+
+
+def test_lex_batch_matches_single(lex_k):
+    a = graphs.rmat(14, seed=5, weight_seed=6)
+    g = DeviceGraph.from_matrix(a)
+    try:
+        srcs = graphs.pick_sources(a.indptr, 6, seed=3)
+        stats, dist = g.solve_batch(srcs, 0.1, concurrency=3)
+        for i, s in enumerate(srcs):
+            st = g.solve(int(s), 0.1)
+            assert np.array_equal(_bits(dist[i]), _bits(g.result_dense()))
+            assert (stats[i].outer_iterations, stats[i].inner_phases) == (st.outer_iterations, st.inner_phases)
+    finally:
+        g.close()
