@@ -74,6 +74,9 @@ typedef struct ds_prep_info {
     int32_t dist_mode;        /* DS_MODE_*                                */
     int32_t frac_bits;        /* fixed-point scale (DS_MODE_FIXED32)      */
     double prepare_ms;        /* device time of the split                 */
+    int32_t sub_buckets;      /* internal buckets per reference bucket (1 = the
+                                 reference's schedule; >1 = lex mode)       */
+    int32_t reserved;
 } ds_prep_info;
 
 typedef struct ds_stats {

@@ -42,6 +42,8 @@ class PrepInfo(ctypes.Structure):
         ("dist_mode", ctypes.c_int32),
         ("frac_bits", ctypes.c_int32),
         ("prepare_ms", ctypes.c_double),
+        ("sub_buckets", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

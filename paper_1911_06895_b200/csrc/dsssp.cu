@@ -218,6 +218,7 @@ struct ds_graph {
     long long ceiling = 0;
     double prep_ms = 0;
     double overflow_delta = NAN;  // delta whose fixed-point solve overflowed
+    double lexfail_delta = NAN;   // delta whose lex-mode keys went out of range
     long long* Lptr = nullptr;
     long long* Hptr = nullptr;
     void* Ledges = nullptr;
@@ -1300,7 +1301,7 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     const bool want_f64 = (flags & DS_FLAG_FORCE_F64) || (delta == g->overflow_delta);
     const char* lx = getenv("DS_LEX");
     const char* lk = getenv("DS_LEX_K");
-    const bool no_lex = (flags & DS_FLAG_NO_LEX) != 0 || (lx && atoi(lx) == 0);
+    const bool no_lex = (flags & DS_FLAG_NO_LEX) != 0 || (lx && atoi(lx) == 0) || delta == g->lexfail_delta;
     const int want_k = lk ? atoi(lk) : 0;  // 0 = auto
     if (g->prepared && g->delta == delta && (g->mode == DS_MODE_F64) == want_f64 && g->no_lex == no_lex &&
         g->want_k == want_k)
@@ -1496,6 +1497,8 @@ extern "C" int ds_graph_prepare(ds_graph* g, double delta, uint32_t flags, ds_pr
         info->dist_mode = g->mode;
         info->frac_bits = g->frac;
         info->prepare_ms = g->prep_ms;
+        info->sub_buckets = g->lex ? g->ksub : 1;
+        info->reserved = 0;
     }
     return DS_OK;
 }
@@ -1586,6 +1589,9 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         p.ksub_log2 = __builtin_ctz((unsigned)g->ksub);
         p.WD = g->WD;
         if (g->lex) p.big_light = p.big_heavy = ~0ull;  // no giant-push handoff (state not resumable)
+        if (getenv("DS_DEBUG_PREP"))
+            fprintf(stderr, "[ds] launch: lex=%d ksub=%d WD=%u nL=%lld nH=%lld refL=%lld mode=%d small=%d\n",
+                    p.lex, g->ksub, p.WD, g->nL, g->nH, g->refL, g->mode, (int)g->small);
         if (g->mode == DS_MODE_FIXED32) {
             const double W = std::isfinite(g->minH) ? ldexp(g->minH, g->frac) : 0.0;
             p.min_heavy = (unsigned long long)W;  // exact: every weight is k * 2^-frac
@@ -1703,6 +1709,7 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         }
     }
     *dev_status = c.status;
+    if (c.status == 0 && c.lexsat) *dev_status = kDevLexFail;
     return DS_OK;
 }
 
@@ -1753,6 +1760,13 @@ extern "C" int ds_sssp(ds_graph* g, int64_t source, double delta, uint32_t flags
         rc = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, x, source, full_grid(g), &st)
                                         : launch_solve<ModeF64>(g, x, source, full_grid(g), &st);
         if (rc) return rc;
+        if (st == kDevLexFail) {
+            // lex keys out of range (D >= 2^26, a saturated final hop count or
+            // a rounding corner): redo with the reference's bucket schedule
+            if (delta == g->lexfail_delta) return set_err(DS_ECUDA, "unexpected lex failure");
+            g->lexfail_delta = delta;
+            continue;
+        }
         if (st == kDevOverflow) {
             // a fixed-point distance would exceed 32 bits: redo in binary64
             g->overflow_delta = delta;
@@ -1896,8 +1910,8 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
             int st = 0;
             int r = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, x, sources[i], grid, &st)
                                                : launch_solve<ModeF64>(g, x, sources[i], grid, &st);
-            if (r == DS_OK && st == kDevOverflow) {
-                redo[t].push_back(i);  // rerun in binary64 after the batch
+            if (r == DS_OK && (st == kDevOverflow || st == kDevLexFail)) {
+                redo[t].push_back(i);  // rerun (binary64 / reference schedule) after the batch
                 continue;
             }
             if (r == DS_OK && st == DS_ENOCONVERGE)
@@ -1952,7 +1966,6 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
         for (long long i : redo[t]) {
             ds_stats one{};
             if ((rc = ds_sssp(g, sources[i], delta, flags, &one))) return rc;
-            one.fallbacks = 1;
             if (stats) stats[i] = one;
             if (dist_out) {
                 CK(cudaMemcpyAsync(dist_out + i * n, g->out, sizeof(double) * n, cudaMemcpyDefault,
@@ -2096,7 +2109,7 @@ extern "C" int ds_graph_download(ds_graph* g, int64_t* indptr, int32_t* col, flo
     if (col && g->nnz > 0) CK(cudaMemcpyAsync(col, g->col, sizeof(int) * g->nnz, cudaMemcpyDefault, g->stream));
     if (val && g->nnz > 0) {
         float* tmp = nullptr;
-        CK(cudaMalloc(&tmp, sizeof(float) * g->nnz));
+        CK((cudaMalloc)((void**)&tmp, sizeof(float) * g->nnz));
         int* bad = reinterpret_cast<int*>(g->pstat);
         CK(cudaMemsetAsync(bad, 0, sizeof(int), g->stream));
         k_download_w<<<elementwise_grid(g), 256, 0, g->stream>>>(g->w, tmp, g->nnz, bad);
@@ -2105,7 +2118,7 @@ extern "C" int ds_graph_download(ds_graph* g, int64_t* indptr, int32_t* col, flo
         int h = 0;
         CK(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
         CK(cudaStreamSynchronize(g->stream));
-        cudaFree(tmp);
+        (cudaFree)(tmp);  // not pooled: a one-off nnz-sized temporary
         if (h) return set_err(DS_EINVAL, "weights are not float32-exact");
     }
     CK(cudaStreamSynchronize(g->stream));

@@ -155,6 +155,7 @@ struct ModeF64 {
 constexpr int kHopBits = 6;
 constexpr unsigned kHopMask = (1u << kHopBits) - 1;
 constexpr unsigned long long kLexDLimit = (1ull << (32 - kHopBits)) - 1;
+constexpr unsigned kLexSat = (unsigned)(kLexDLimit << kHopBits);  // < INF (0xFFFFFFFF)
 
 template <class M>
 struct KParams;
@@ -165,10 +166,18 @@ __device__ __forceinline__ bool padd(const KParams<M>& p, typename M::D ku, cons
                                      typename M::D hd, typename M::D& nd) {
     if constexpr (LEX && std::is_same<M, ModeFixed>::value) {
         // 32-bit: D < 2^26 and every weight W < 2^26 (checked at prepare)
+        // Hops saturate at kHopMask: a saturated key still orders below every
+        // longer walk of the same distance, and only a FINAL key of the
+        // bucket at kHopMask (checked at its S capture) is unusable.
+        // A sum beyond the key range becomes kLexSat: larger than every real
+        // key (so any real path replaces it) but still "reached"; should one
+        // survive until the solver reaches it, the solve reruns without lex
+        // (its true distance is not representable).
         const unsigned s = (ku >> kHopBits) + e.y;
-        const unsigned h = (e.y <= p.WD && s < hd) ? (ku & kHopMask) + 1u : 0u;
-        nd = (s << kHopBits) | h;
-        return s < (unsigned)kLexDLimit && h <= kHopMask;
+        const unsigned hu = ku & kHopMask;
+        const unsigned h = (e.y <= p.WD && s < hd) ? hu + (hu < kHopMask ? 1u : 0u) : 0u;
+        nd = s < (unsigned)kLexDLimit ? (s << kHopBits) | h : kLexSat;
+        return true;
     }
     return M::add(ku, e, nd);
 }
@@ -288,12 +297,14 @@ struct Ctl {
     unsigned long long h_phases, h_re, h_pp, h_done, h_status, h_escanned;
     unsigned long long hh_re, hh_done, hh_status;
     unsigned long long t_enter, t_exit;  // DS_TRACE: kernel entry / last CTA's finalize end
+    unsigned lexsat;  // lex mode: a final key held an out-of-range sum (rerun without lex)
 };
 
 enum : int { POS_FRESH = 0, POS_BUCKET = 1, POS_PHASE = 2, POS_AFTER_LIGHT = 3, POS_HEAVY = 4,
              POS_AFTER_HEAVY = 5 };
 
 constexpr int kDevOverflow = 100;  // internal status: fixed-point overflow
+constexpr int kDevLexFail = 101;   // internal status: lex keys out of range (rerun without lex)
 
 // Pull schedule of one CSR (light or heavy) in solver order: the rows with
 // at least one edge, their offsets, the row holding the first edge of every
@@ -1177,7 +1188,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     // DS_LATE_FLUSH: appends stay in the warp queue across chunks until it
     // is half full, so most chunks skip the reservation round trip
     if (LIGHT) wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
-    if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, 1u);
+    if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, LEX ? 2u : 1u);
 }
 
 // ---------------------------------------------------------------- pull step
@@ -1559,8 +1570,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             M::window(lo, hi, p.frac, LD, HD2);
             if ((unsigned long long)HD - LD > (unsigned long long)p.WD + 1ull) {
                 // a reference-heavy edge could land inside its own bucket (a
-                // rounding corner of fl(i*delta)): leave to the exact f64 mode
-                status = kDevOverflow;
+                // rounding corner of fl(i*delta)): rerun with the reference schedule
+                status = kDevLexFail;
                 break;
             }
             const long long ridx = idx >> p.ksub_log2;
@@ -1588,6 +1599,10 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             if (fc == 0) {
                 const unsigned long long nm = ldcg(&prev()->next_min);
                 if (nm == ~0ull) break;  // nothing stored beyond: done
+                if (kLex && nm >= kLexSat) {  // only out-of-range sums remain: not representable
+                    status = kDevLexFail;
+                    break;
+                }
                 if (kLex) {
                     // next internal bucket: the reference bucket of the value,
                     // then the sub-window holding it
@@ -1729,8 +1744,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 relax_step<M, true, false, kSum, false, kLex>(p, sm, &c->slot[st % 3], E, re >> kPackShift,
                                                              p.Ledges, H, p.F[pp], p.fbits[phases & 1], HD);
                 if (!end_step(1, E)) return;
-                if (ldcg(&prev()->flags) & 1u) {
-                    status = kDevOverflow;
+                if (const unsigned fl = ldcg(&prev()->flags) & 3u) {
+                    status = (fl & 2u) ? kDevLexFail : kDevOverflow;
                     break;
                 }
                 nf = ldcg(&prev()->append_count);
@@ -1804,8 +1819,14 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                                               p.Hptr, nullptr, nullptr, nullptr);
                 if (!end_step(3, scount)) return;
                 re = ldcg(&prev()->re_packed);
-                if (kLex && threadIdx.x == 0)
-                    sm.lx.hop_acc = max(sm.lx.hop_acc, ldcg(&prev()->hopmax));
+                if (kLex) {
+                    const unsigned hm = ldcg(&prev()->hopmax);
+                    if (hm >= kHopMask) {  // a final hop count saturated: not representable
+                        status = kDevLexFail;
+                        break;
+                    }
+                    if (threadIdx.x == 0) sm.lx.hop_acc = max(sm.lx.hop_acc, hm);
+                }
             }
             const unsigned long long E = heavy_done ? 0ull : (re & kMask33);
             hset += re & kMask33;  // S's rows are settled: their heavy edges leave the pull volume
@@ -1840,8 +1861,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                         relax_step<M, false, false, kSum, true, kLex>(p, sm, &c->slot[st % 3], Ep, pre >> kPackShift,
                                                                 p.Hedges, H, nullptr, nullptr, HD);
                         if (!end_step(12, Ep)) return;
-                        if (ldcg(&prev()->flags) & 1u) {
-                            status = kDevOverflow;
+                        if (const unsigned fl = ldcg(&prev()->flags) & 3u) {
+                            status = (fl & 2u) ? kDevLexFail : kDevOverflow;
                             break;
                         }
                     }
@@ -1870,8 +1891,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 relax_step<M, false, false, kSum, false, kLex>(p, sm, &c->slot[st % 3], E, re >> kPackShift,
                                                               p.Hedges, H, nullptr, nullptr, HD);
                 if (!end_step(4, E)) return;
-                if (ldcg(&prev()->flags) & 1u) {
-                    status = kDevOverflow;
+                if (const unsigned fl = ldcg(&prev()->flags) & 3u) {
+                    status = (fl & 2u) ? kDevLexFail : kDevOverflow;
                     break;
                 }
             }
@@ -1939,6 +1960,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 d[j] = sv[j] < n_scan ? __ldcg(p.dist + sv[j]) : M::INF;
+                if (kLex && d[j] == (D)kLexSat) atomicOr(&c->lexsat, 1u);
                 if (kLex && d[j] != M::INF) d[j] >>= kHopBits;  // key -> distance
             }
             double o[8];
