@@ -1888,7 +1888,7 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
     std::atomic<long long> next(0);
     std::vector<int> err(T, DS_OK);
     std::vector<std::string> msg(T);
-    std::vector<std::vector<long long>> redo(T);
+    std::vector<std::vector<std::pair<long long, int>>> redo(T);  // (source index, device status)
     auto worker = [&](int t) {
         cudaSetDevice(g->device);
         SolveCtx& x = ctx[t];
@@ -1911,7 +1911,7 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
             int r = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, x, sources[i], grid, &st)
                                                : launch_solve<ModeF64>(g, x, sources[i], grid, &st);
             if (r == DS_OK && (st == kDevOverflow || st == kDevLexFail)) {
-                redo[t].push_back(i);  // rerun (binary64 / reference schedule) after the batch
+                redo[t].push_back({i, st});  // rerun (binary64 / reference schedule) after the batch
                 continue;
             }
             if (r == DS_OK && st == DS_ENOCONVERGE)
@@ -1963,9 +1963,10 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
     }
     g->have_result = false;  // batch results are delivered through dist_out
     for (int t = 0; t < T; ++t)
-        for (long long i : redo[t]) {
+        for (const auto& [i, why] : redo[t]) {
             ds_stats one{};
             if ((rc = ds_sssp(g, sources[i], delta, flags, &one))) return rc;
+            if (why == kDevOverflow) one.fallbacks = 1;  // its fixed-point solve overflowed in the batch
             if (stats) stats[i] = one;
             if (dist_out) {
                 CK(cudaMemcpyAsync(dist_out + i * n, g->out, sizeof(double) * n, cudaMemcpyDefault,

@@ -204,7 +204,11 @@ constexpr int kRelPer = kChunk / 32;
 #ifndef DS_LIST_PER
 #define DS_LIST_PER 2
 #endif
-constexpr int kListPer = DS_LIST_PER;  // capture (list): entries per lane
+constexpr int kListPer = DS_LIST_PER;  // capture (range): entries per lane per round
+#ifndef DS_CAP_PER
+#define DS_CAP_PER DS_LIST_PER
+#endif
+constexpr int kCapPer = DS_CAP_PER;  // capture (list): entries per lane per round
 #ifndef DS_QUEUE
 #define DS_QUEUE 256
 #endif
@@ -416,6 +420,7 @@ struct Smem {
     int ok;
     LexAcc lx;
 };
+static_assert(kWarps <= 32, "one warp scans the CTA's per-warp totals");
 
 // ---------------------------------------------------------------- warp / block utils
 
@@ -657,6 +662,53 @@ __device__ __forceinline__ void capture_emit(const KParams<M>& p, StepSlot* slot
     }
 }
 
+// CTA-cooperative form of capture_emit: every warp of the CTA calls it once
+// per round; the warps' totals are scanned in shared memory and the CTA makes
+// ONE packed reservation for all of them.  (Per-warp reservations all hit one
+// counter: at R-MAT 24 they were ~16% of the solver's stall samples.)
+template <class M, int PER>
+__device__ __forceinline__ void capture_emit_cta(const KParams<M>& p, Smem<typename M::D>& sm,
+                                                 StepSlot* slot, int lane, int wib,
+                                                 const typename M::D (&dv)[PER],
+                                                 const long long (&off)[PER], const long long (&deg)[PER]) {
+    unsigned long long packed = 0;  // (count << 48) | degree within the warp chunk
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+        if (deg[j] > 0) packed += (1ull << 48) + (unsigned long long)deg[j];
+    const unsigned long long incl = warp_incl_scan(packed, lane);
+    if (lane == 31) sm.red[wib] = incl;
+    __syncthreads();
+    if (wib == 0) {
+        const unsigned long long wt = lane < kWarps ? sm.red[lane] : 0ull;
+        const unsigned long long wi = warp_incl_scan(wt, lane);
+        const unsigned long long all = __shfl_sync(0xffffffffu, wi, 31);
+        unsigned long long r = 0;
+        if (lane == 31 && all) r = atomicAdd(&slot->re_packed, ((all >> 48) << kPackShift) | (all & kMask48));
+        r = __shfl_sync(0xffffffffu, r, 31);
+        const unsigned long long we = wi - wt;  // warps before this one
+        if (lane < kWarps) {
+            sm.red[lane] = (r >> kPackShift) + (we >> 48);  // first entry rank
+            sm.red2[lane] = (r & kMask33) + (we & kMask48);  // first edge prefix
+        }
+    }
+    __syncthreads();
+    const unsigned long long excl = incl - packed;
+    unsigned long long rank = sm.red[wib] + (excl >> 48);
+    unsigned long long pre = sm.red2[wib] + (excl & kMask48);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        if (deg[j] > 0) {
+            p.Rent[rank] = make_uint2((unsigned)pre, (unsigned)(off[j] - (long long)pre));
+            p.Rd[rank] = dv[j];
+            const unsigned long long t0 = (pre + kChunk - 1) / kChunk;
+            const unsigned long long t1 = (pre + (unsigned long long)deg[j] - 1) / kChunk;
+            for (unsigned long long t = t0; t <= t1; ++t) p.chunk_start[t] = (unsigned)rank;
+            ++rank;
+            pre += (unsigned long long)deg[j];
+        }
+    }
+}
+
 template <class D>
 __device__ __forceinline__ void load_run(const D* p, D (&out)[kRangePer]);
 template <>
@@ -828,25 +880,29 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem<D>& ws = sm.w[wib];
     unsigned qn = 0;
-    const unsigned long long per_chunk = 32ull * kListPer;
+    const unsigned long long per_chunk = 32ull * kCapPer;
     const unsigned long long nchunk = (count + per_chunk - 1) / per_chunk;
     // LOCALW: only this CTA's warps take part (block-local small-frontier mode)
-    const unsigned long long gw = LOCALW ? wib : (unsigned long long)blockIdx.x * kWarps + wib;
+    // CTA-uniform rounds (capture_emit_cta synchronises the CTA's warps):
+    // warp w of the CTA takes chunk cbase + w
+    const unsigned long long cb0 = LOCALW ? 0ull : (unsigned long long)blockIdx.x * kWarps;
     const unsigned long long nw = LOCALW ? kWarps : (unsigned long long)gridDim.x * kWarps;
-    for (unsigned long long c = gw; c < nchunk; c += nw) {
-        int vtx[kListPer];
-        bool in[kListPer];
-        D dv[kListPer];
+    unsigned hop_cta = 0;  // lex S capture: largest hop count seen by this warp
+    for (unsigned long long cbase = cb0; cbase < nchunk; cbase += nw) {
+        const unsigned long long c = cbase + wib;
+        int vtx[kCapPer];
+        bool in[kCapPer];
+        D dv[kCapPer];
 #pragma unroll
-        for (int j = 0; j < kListPer; ++j) {
+        for (int j = 0; j < kCapPer; ++j) {
             const unsigned long long idx = c * per_chunk + lane + 32ull * j;
-            in[j] = idx < count;
+            in[j] = c < nchunk && idx < count;
             vtx[j] = in[j] ? ldcg(list + idx) : 0;
             if (VALS) dv[j] = in[j] ? __ldcg(vals + idx) : (D)0;
         }
-        long long off[kListPer], deg[kListPer];
+        long long off[kCapPer], deg[kCapPer];
 #pragma unroll
-        for (int j = 0; j < kListPer; ++j) {
+        for (int j = 0; j < kCapPer; ++j) {
             if (VALS) {
                 if (in[j]) p.dist[vtx[j]] = dv[j];
             } else {
@@ -860,28 +916,29 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
             // lex mode, S capture of an internal bucket: its largest hop count
             // (S holds the bucket's final keys)
             if (p.lex) {
-                unsigned hm = 0;
 #pragma unroll
-                for (int j = 0; j < kListPer; ++j)
-                    if (in[j]) hm = max(hm, (unsigned)dv[j] & kHopMask);
-#pragma unroll
-                for (int o = 16; o; o >>= 1) hm = max(hm, __shfl_xor_sync(0xffffffffu, hm, o));
-                if (lane == 0 && hm) atomicMax(&slot->hopmax, hm);
+                for (int j = 0; j < kCapPer; ++j)
+                    if (in[j]) hop_cta = max(hop_cta, (unsigned)dv[j] & kHopMask);
             }
         }
         if (APPEND_S) {
-            bool news[kListPer];
+            bool news[kCapPer];
 #pragma unroll
-            for (int j = 0; j < kListPer; ++j) news[j] = in[j] && claim_bit(p.sbits, (unsigned)vtx[j]);
+            for (int j = 0; j < kCapPer; ++j) news[j] = in[j] && claim_bit(p.sbits, (unsigned)vtx[j]);
 #pragma unroll
-            for (int j = 0; j < kListPer; ++j)
+            for (int j = 0; j < kCapPer; ++j)
                 wq_push<D, false>(ws.q, queue_vals(ws), qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
             if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
                 wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
         }
-        capture_emit<M, kListPer>(p, slot, lane, dv, off, deg);
+        capture_emit_cta<M, kCapPer>(p, sm, slot, lane, wib, dv, off, deg);
     }
     if (APPEND_S) wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
+    if (!APPEND_S && !VALS && std::is_same<M, ModeFixed>::value && p.lex) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) hop_cta = max(hop_cta, __shfl_xor_sync(0xffffffffu, hop_cta, o));
+        if (lane == 0 && hop_cta) atomicMax(&slot->hopmax, hop_cta);  // once per warp and capture
+    }
 }
 
 // ---------------------------------------------------------------- relax step (push)
