@@ -348,12 +348,22 @@ def partitioned_arm(args):
                                                    partition_bounds)
 
     ws, rank, local = dist_env()
+    ndev = torch.cuda.device_count()
+    shared = ndev < ws  # fewer GPUs than ranks (a 1-GPU lease): ranks share devices
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
-    dist.init_process_group("nccl", rank=rank, world_size=ws, device_id=dev)
-    scale = args.scale if args.scale_given else 27
+    if shared:
+        # NCCL needs one GPU per rank: exchange over gloo through host memory
+        # (the ranks meet only in host-side collectives, never inside kernels)
+        dist.init_process_group("gloo", rank=rank, world_size=ws)
+    else:
+        dist.init_process_group("nccl", rank=rank, world_size=ws, device_id=dev)
+    xdev = "cpu" if shared else "cuda"
+    # R-MAT 27 needs ~100 GB per rank while generating: one rank per GPU
+    scale = args.scale if args.scale_given else (24 if shared else 27)
     nsrc = args.batch if "--batch" in sys.argv else 16
     delta = args.delta
     g = DeviceGraph.rmat(scale, args.edge_factor, 1, 2, device=local)
@@ -376,9 +386,9 @@ def partitioned_arm(args):
         m_rep += g.solve(s, delta).edges_reached
     e1.record()
     torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    t = torch.tensor([e0.elapsed_time(e1)], device=xdev if shared else dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    mm = torch.tensor([float(m_rep)], dtype=torch.float64, device=dev)
+    mm = torch.tensor([float(m_rep)], dtype=torch.float64, device=xdev if shared else dev)
     dist.all_reduce(mm)
     replicas = {"value": float(mm.item()) / (float(t.item()) * 1e-3) / 1e9, "unit": UNIT,
                 "ms_per_step": float(t.item()), "sources_per_rank": len(mine)}
@@ -389,7 +399,7 @@ def partitioned_arm(args):
     b = partition_bounds(n, ws)
     shard = DeviceShard.from_graph(g, b[rank], b[rank + 1])
     g.close()
-    solver = PartitionedDeltaStepping(shard, n, dist, "cuda")
+    solver = PartitionedDeltaStepping(shard, n, dist, xdev)
     mydeg = torch.from_numpy(deg[b[rank]:b[rank + 1]].astype(np.int64)).to(dev)
 
     for w in range(args.warmup):
@@ -397,8 +407,13 @@ def partitioned_arm(args):
     # parity of pool[0] against rank 0's single-GPU solve
     r0 = solver.solve(srcs[0], delta, on_device=True)
     sizes = [b[i + 1] - b[i] for i in range(ws)]
-    parts = [torch.empty(sz, dtype=torch.float64, device=dev) for sz in sizes]
-    dist.all_gather(parts, r0.local.contiguous())
+    xd = torch.device(xdev if xdev == "cpu" else dev)
+    m = max(sizes)
+    mine_local = torch.full((m,), float("inf"), dtype=torch.float64, device=xd)
+    mine_local[: sizes[rank]] = r0.local.to(xd)
+    parts = [torch.empty(m, dtype=torch.float64, device=xd) for _ in sizes]
+    dist.all_gather(parts, mine_local)
+    parts = [p[:sz] for p, sz in zip(parts, sizes)]
     parity = None
     if rank == 0:
         got = torch.cat(parts).cpu().numpy()
@@ -418,9 +433,9 @@ def partitioned_arm(args):
     e1.record()
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    t = torch.tensor([e0.elapsed_time(e1)], device=xdev if shared else dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    m = torch.tensor([float(m_local)], dtype=torch.float64, device=dev)
+    m = torch.tensor([float(m_local)], dtype=torch.float64, device=xdev if shared else dev)
     dist.all_reduce(m)
     t_ms = float(t.item())
     value = float(m.item()) / (t_ms * 1e-3) / 1e9
@@ -432,7 +447,9 @@ def partitioned_arm(args):
             "data": "synthetic (seeded R-MAT, generated on device)",
             "config": {"workload": f"rmat{scale}_ef{args.edge_factor}_delta{delta}",
                        "n": n, "nnz": nnz, "sources_per_step": len(srcs),
-                       "parallelism": f"1-D vertex partition x{ws}, NCCL all-gather per light phase",
+                       "parallelism": (f"1-D vertex partition x{ws}, "
+                                       + ("gloo exchange, ranks sharing %d GPU(s)" % ndev if shared
+                                          else "NCCL all-gather per light phase")),
                        "l2": "inputs larger than L2"},
             "parity": parity,
             "replicas": replicas,

@@ -216,34 +216,43 @@ class PartitionedDeltaStepping:
         self.world = pg.get_world_size()
 
     # -- collectives ---------------------------------------------------
+    # Per light phase the protocol needs exactly two collectives and one host
+    # read: a tiny all-gather of every rank's (count, flag) pair -- the counts
+    # size the frontier exchange, the flag carries a fixed-point overflow --
+    # and one all-gather of the packed (id, value) frontier entries.
     def _allreduce(self, value, op, dtype):
         t = self.torch.tensor([value], dtype=dtype, device=self.xdev)
         self.pg.all_reduce(t, op=op)
         return t.item()
 
-    def _allgather_frontier(self, ids, vals, count: int):
+    def _exchange_meta(self, *vals) -> np.ndarray:
+        """All-gather a few int64 scalars per rank -> (world, k) host array."""
         torch = self.torch
-        c = torch.tensor([count], dtype=torch.int64, device=self.xdev)
-        cs = [torch.zeros_like(c) for _ in range(self.world)]
-        self.pg.all_gather(cs, c)
-        counts = [int(x.item()) for x in cs]
+        t = torch.tensor([int(v) for v in vals], dtype=torch.int64, device=self.xdev)
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        self.pg.all_gather(parts, t)
+        return torch.stack(parts).cpu().numpy()
+
+    def _gather_entries(self, ids, vals, counts):
+        """All-gather every rank's frontier (ids int32, u64 values as int64)
+        as ONE padded (2, max count) int64 tensor per rank."""
+        torch = self.torch
+        counts = [int(c) for c in counts]
         total = sum(counts)
-        dev = ids.device if count else getattr(self.shard, "device", self.xdev)
+        dev = ids.device if counts[self.pg.get_rank()] else getattr(self.shard, "device", self.xdev)
         if total == 0:
             return (torch.empty(0, dtype=torch.int32, device=dev),
                     torch.empty(0, dtype=torch.int64, device=dev), 0)
         m = max(counts)
-        pid = torch.zeros(m, dtype=torch.int32, device=self.xdev)
-        pval = torch.zeros(m, dtype=torch.int64, device=self.xdev)
-        if count:
-            pid[:count] = ids.to(self.xdev)
-            pval[:count] = vals.to(self.xdev)
-        gi = [torch.empty_like(pid) for _ in range(self.world)]
-        gv = [torch.empty_like(pval) for _ in range(self.world)]
-        self.pg.all_gather(gi, pid)
-        self.pg.all_gather(gv, pval)
-        out_i = torch.cat([g[:k] for g, k in zip(gi, counts)]).to(dev)
-        out_v = torch.cat([g[:k] for g, k in zip(gv, counts)]).to(dev)
+        mine = counts[self.pg.get_rank()]
+        buf = torch.zeros((2, m), dtype=torch.int64, device=self.xdev)
+        if mine:
+            buf[0, :mine] = ids.to(self.xdev).to(torch.int64)
+            buf[1, :mine] = vals.to(self.xdev)
+        outs = [torch.empty_like(buf) for _ in range(self.world)]
+        self.pg.all_gather(outs, buf)
+        out_i = torch.cat([o[0, :k] for o, k in zip(outs, counts)]).to(torch.int32).to(dev)
+        out_v = torch.cat([o[1, :k] for o, k in zip(outs, counts)]).to(dev)
         return out_i, out_v, total
 
     # -- solve ---------------------------------------------------------
@@ -301,24 +310,26 @@ class PartitionedDeltaStepping:
         return math.ldexp(float(v), -frac) if mode == MODE_FIXED32 else _bits_f64(v)
 
     def _run(self, source, delta, mode, frac, ceiling, on_device=False):
-        R = self.pg.ReduceOp
-        torch = self.torch
         sh = self.shard
         sh.prepare(delta, mode, frac)
         sh.begin(source)
         idx, phases, visited, exchanged = 0, 0, 0, 0
+        heavy_ovf = 0  # the previous bucket's heavy-step overflow, carried in the next scan's meta
         while True:
             L, H = self._window(idx, delta, mode, frac)
             ids, vals, cnt, nmin = sh.scan(L, H)
-            fc = int(self._allreduce(cnt, R.SUM, torch.int64))
-            nm = int(self._allreduce(I64_NONE if nmin == NONE else nmin, R.MIN, torch.int64))
+            meta = self._exchange_meta(cnt, I64_NONE if nmin == NONE else nmin, heavy_ovf)
+            if meta[:, 2].max():
+                return None  # a fixed-point sum overflowed on some rank: exact f64 rerun
+            fc = int(meta[:, 0].sum())
+            nm = int(meta[:, 1].min())
             if fc == 0:
                 if nm == I64_NONE:
                     break  # nothing stored beyond the window: done
                 idx = bucket_index_of(self._value(nm, mode, frac), delta)
                 continue
             visited += 1
-            F, Fv, nf = self._allgather_frontier(ids, vals, cnt)
+            F, Fv, nf = self._gather_entries(ids, vals, meta[:, 0])
             exchanged += nf
             sh.s_add(F, Fv, nf)
             while True:  # light phases (sssp.py:292-301)
@@ -327,16 +338,15 @@ class PartitionedDeltaStepping:
                     raise RuntimeError(f"light phase count exceeded ceiling {ceiling}; "
                                        "relaxation is not converging")
                 nids, nvals, ncnt, ovf = sh.relax_light(F, Fv, nf, H)
-                if self._allreduce(int(ovf), R.MAX, torch.int64):
+                meta = self._exchange_meta(ncnt, int(ovf))
+                if meta[:, 1].max():
                     return None
-                F, Fv, nf = self._allgather_frontier(nids, nvals, ncnt)
+                F, Fv, nf = self._gather_entries(nids, nvals, meta[:, 0])
                 exchanged += nf
                 if nf == 0:
                     break
                 sh.s_add(F, Fv, nf)
-            ovf = sh.relax_heavy()  # S values are final; no exchange needed
-            if self._allreduce(int(ovf), R.MAX, torch.int64):
-                return None
+            heavy_ovf = int(sh.relax_heavy())  # S values are final; no exchange needed
             idx += 1
         local = sh.result(on_device=True) if on_device else sh.result()
         return local, phases, visited, exchanged

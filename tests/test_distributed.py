@@ -116,3 +116,21 @@ def test_partitioned_protocol_world2_cpu_gloo():
 @pytest.mark.gpu
 def test_partitioned_device_shards_world2_gloo():
     _run(use_gpu=True)
+
+
+def test_bench_self_spawns_ranks_on_cpu():
+    # `python bench.py --gpus 2` outside torchrun re-launches itself under
+    # torch.distributed.run with two ranks; the reference arm runs on rank 0
+    # only (the CPU-only arm: no GPU needed here)
+    import json
+    import subprocess
+
+    r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--steps", "1", "--warmup", "0", "--scale", "10", "--scale", "10",
+                        "--no-python-ref"], capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    assert d["config"]["workload"] == "rmat10_ef16_delta0.1"
