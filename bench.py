@@ -71,7 +71,7 @@ def parse():
     ap.add_argument("--batch", type=int, default=64,
                     help="sources per step (per rank); default = the BASELINE's 64-source pool")
     ap.add_argument("--sources", type=int, default=64, help="source pool (BASELINE: 64)")
-    ap.add_argument("--concurrency", type=int, default=2,
+    ap.add_argument("--concurrency", type=int, default=4,
                     help="sources in flight per GPU (ds_sssp_batch contexts; 1 = one at a time)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -1846,8 +1846,10 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
         // graphs leave a full grid latency-bound, so 8 solves in flight pay
         // (R-MAT 18 7.0 -> 18.1 GTEPS, R-MAT 19 13.0 -> 29.4, grid 2048^2
         // 197 -> 50 ms/source); from R-MAT 20 (30 M edges) on, two do
-        // (R-MAT 20 23.1 -> 39.4, R-MAT 24 76.8 -> 83.5; 8 would cost 10-48%)
-        T = (g->small || g->nnz < (24LL << 20)) ? 8 : 2;
+        // (R-MAT 20 23.1 -> 39.4, R-MAT 24 76.8 -> 83.5; 8 would cost 10-48%).
+        // Round 2 (heavy gather, lex mode): R-MAT 24 peaks at 4 in flight
+        // (bench: 106 / 123 / 125-133 / 100 GTEPS at 2 / 3 / 4 / 6)
+        T = (g->small || g->nnz < (24LL << 20)) ? 8 : 4;
         if (const char* e = getenv("DS_BATCH_CONC")) T = std::max(1, atoi(e));
     }
     T = (int)std::min<long long>({(long long)T, (long long)k, 8LL, (long long)g->nsm});
