@@ -274,6 +274,9 @@ struct ds_graph {
     bool small = false;  // use the block-local-phase kernel (high-diameter graphs)
     size_t persist_bytes = 0, max_window = 0;
     unsigned long long* trace = nullptr;  // DS_TRACE=1: per-step timeline
+    unsigned long long* cta_done = nullptr;  // DS_TRACE=2: per-step per-CTA finish times
+    size_t cta_done_words = 0;
+    unsigned cta_done_grid = 0;
     unsigned long long trace_cap = 0;
     unsigned long long trace_len = 0;
     long long trace_t0 = 0;
@@ -322,7 +325,7 @@ static void free_all(ds_graph* g) {
                     g->planL.rowid, g->planL.cptr, g->planL.chunk_row, g->planL.span,
                     g->planH.rowid, g->planH.cptr, g->planH.chunk_row, g->planH.span,
                     g->Rbase,  g->Rd,   g->chunk_start, g->order, g->perm, g->sdeg, g->ctl,
-                    g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace, g->csum};
+                    g->pstat,  g->out,  g->cidx,  g->ccount, g->cub_tmp, g->trace, g->csum, g->cta_done};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (SolveCtx* x : g->extra) {
@@ -1622,6 +1625,17 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     unsigned long long* trace = x.traced ? g->trace : nullptr;
     p.trace = trace;
     p.trace_cap = g->trace_cap;
+    p.cta_done = nullptr;
+    if (const char* tr = getenv("DS_TRACE"); tr && atoi(tr) == 2 && trace) {
+        const size_t words = (size_t)g->trace_cap * (size_t)grid;
+        if (g->cta_done_words < words) {
+            if (g->cta_done) (cudaFree)(g->cta_done);
+            CK((cudaMalloc)((void**)&g->cta_done, sizeof(unsigned long long) * words));
+            g->cta_done_words = words;
+        }
+        g->cta_done_grid = grid;
+        p.cta_done = g->cta_done;
+    }
     if (trace) CK(cudaMemsetAsync(trace, 0, 2 * sizeof(unsigned long long) * g->trace_cap, x.stream));
     CK(cudaMemsetAsync(x.ctl, 0, sizeof(Ctl), x.stream));
     cudaLaunchConfig_t cfg = {};
@@ -2165,6 +2179,19 @@ extern "C" int64_t ds_debug_trace(ds_graph* g, uint64_t* out, int64_t cap) {
                             cudaMemcpyDeviceToHost) != cudaSuccess)
         return 0;
     return m;
+}
+
+// DS_TRACE=2 diagnostics: per step, the time each CTA's warps finished it
+// (out[0] = grid size, then steps x grid words); returns the words written.
+extern "C" int64_t ds_debug_cta_times(ds_graph* g, uint64_t* out, int64_t cap) {
+    if (!g || !g->cta_done || cap < 1) return 0;
+    DeviceGuard guard(g->device);
+    const long long words = std::min((long long)g->trace_len * g->cta_done_grid, (long long)cap - 1);
+    out[0] = g->cta_done_grid;
+    if (words > 0 && cudaMemcpy(out + 1, g->cta_done, sizeof(unsigned long long) * words,
+                                cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    return words;
 }
 
 int ds_internal_graph_csr(ds_graph* g, long long** indptr, int** col, double** w, long long* n,
