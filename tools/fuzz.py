@@ -36,8 +36,31 @@ def make():
     return a
 
 
+base_env = dict(os.environ)
+
+
+def knobs():
+    """Random solver knobs: lex mode forced with ksub 1..8, the heavy gather
+    forced on small graphs (any ratio) or off."""
+    env = dict(base_env)
+    lk = int(rng.integers(0, 5))
+    if lk:
+        env["DS_LEX"] = "1"
+        env["DS_LEX_K"] = str(1 << (lk - 1))
+    hp = int(rng.integers(0, 3))
+    if hp == 1:
+        env["DS_HPULL_MIN"] = "0"
+        env["DS_HPULL_RATIO"] = str(float(rng.choice([0.0, 0.3, 1.0, 3.0])))
+    elif hp == 2:
+        env["DS_HPULL"] = "0"
+    os.environ.clear()
+    os.environ.update(env)
+    return f"lex={env.get('DS_LEX_K', '-')} hpull={hp}"
+
+
 while time.time() < t_end:
     a = make()
+    tag = knobs()
     g = DeviceGraph.from_matrix(a)
     deg = np.diff(a.indptr)
     cands = np.flatnonzero(deg > 0)
@@ -57,7 +80,7 @@ while time.time() < t_end:
         runs += 1
         if not ok:
             fails += 1
-            print(f"FAIL single n={a.n} nnz={a.nnz} s={s} delta={delta!r} skip={skip} f64={f64}", flush=True)
+            print(f"FAIL single n={a.n} nnz={a.nnz} s={s} delta={delta!r} skip={skip} f64={f64} {tag}", flush=True)
     stats, dist = g.solve_batch(srcs, delta, skip_empty_buckets=skip, force_f64=f64,
                                 concurrency=int(rng.integers(1, 4)))
     for i, s in enumerate(srcs):
@@ -67,7 +90,7 @@ while time.time() < t_end:
         runs += 1
         if not ok:
             fails += 1
-            print(f"FAIL batch n={a.n} nnz={a.nnz} s={s} delta={delta!r} skip={skip} f64={f64}", flush=True)
+            print(f"FAIL batch n={a.n} nnz={a.nnz} s={s} delta={delta!r} skip={skip} f64={f64} {tag}", flush=True)
     g.close()
 print(f"fuzz: {runs} solves, {fails} mismatches", flush=True)
 sys.exit(1 if fails else 0)
