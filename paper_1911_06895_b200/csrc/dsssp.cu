@@ -686,31 +686,34 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
     x ^= x >> 33;
     return x;
 }
-__device__ __forceinline__ void triple_hash(unsigned long long a, unsigned long long b,
-                                            unsigned long long w, unsigned long long& h1,
-                                            unsigned long long& h2) {
-    const unsigned long long k = (a << 32) | b;
-    h1 = mix64(k ^ mix64(w + 0x9E3779B97F4A7C15ull));
-    h2 = mix64((k * 0xD6E8FEB86659FD93ull) ^ mix64(w ^ 0x632BE59BD9B4E019ull) ^ 0x5851F42D4C957F2Dull);
+// (u, v, w) and (v, u, w) hashes of one edge; the weight's mixes are shared
+__device__ __forceinline__ void pair_hashes(unsigned long long u, unsigned long long v, unsigned long long w,
+                                            unsigned long long& f1, unsigned long long& f2,
+                                            unsigned long long& r1, unsigned long long& r2) {
+    const unsigned long long mw1 = mix64(w + 0x9E3779B97F4A7C15ull);
+    const unsigned long long mw2 = mix64(w ^ 0x632BE59BD9B4E019ull) ^ 0x5851F42D4C957F2Dull;
+    const unsigned long long kf = (u << 32) | v, kr = (v << 32) | u;
+    f1 += mix64(kf ^ mw1);
+    f2 += mix64((kf * 0xD6E8FEB86659FD93ull) ^ mw2);
+    r1 += mix64(kr ^ mw1);
+    r2 += mix64((kr * 0xD6E8FEB86659FD93ull) ^ mw2);
 }
+// Edge-parallel (a warp per contiguous edge slice, lanes walking indptr like
+// k_split_count): a warp per row left most lanes idle on R-MAT's short rows.
 __global__ void k_symmetry_sums(const long long* indptr, const int* col, const double* w, long long n,
-                                unsigned long long* sums) {
+                                long long nnz, unsigned long long* sums) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long per = ((nnz + nwarps - 1) / nwarps + 31) & ~31LL;
+    const long long e_begin = warp * per, e_end = min(nnz, e_begin + per);
     unsigned long long f1 = 0, f2 = 0, r1 = 0, r2 = 0;
-    for (long long u = warp; u < n; u += nwarps) {
-        const long long a = indptr[u], b = indptr[u + 1];
-        for (long long e = a + lane; e < b; e += 32) {
-            const unsigned long long v = (unsigned)col[e];
-            const unsigned long long wb = (unsigned long long)__double_as_longlong(w[e]);
-            unsigned long long h1, h2;
-            triple_hash((unsigned long long)u, v, wb, h1, h2);
-            f1 += h1;
-            f2 += h2;
-            triple_hash(v, (unsigned long long)u, wb, h1, h2);
-            r1 += h1;
-            r2 += h2;
+    if (e_begin < e_end) {
+        long long r = warp_first_row(indptr, n, e_begin);
+        for (long long e = e_begin + lane; e < e_end; e += 32) {
+            while (__ldg(indptr + r + 1) <= e) ++r;
+            pair_hashes((unsigned long long)r, (unsigned)__ldg(col + e),
+                        (unsigned long long)__double_as_longlong(__ldg(w + e)), f1, f2, r1, r2);
         }
     }
     f1 = warp_sum(f1);
@@ -1022,7 +1025,7 @@ static int check_symmetric(ds_graph* g) {
     CK(cudaMemsetAsync(sums, 0, 4 * sizeof(unsigned long long), g->stream));
     if (g->nnz > 0)
         k_symmetry_sums<<<(unsigned)(g->nsm * 16), 256, 0, g->stream>>>(g->indptr, g->col, g->w, g->n,
-                                                                        sums);
+                                                                        g->nnz, sums);
     CK(cudaGetLastError());
     unsigned long long h[4];
     CK(cudaMemcpyAsync(h, sums, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
