@@ -233,9 +233,11 @@ class PartitionedDeltaStepping:
         self.pg.all_gather(parts, t)
         return torch.stack(parts).cpu().numpy()
 
-    def _gather_entries(self, ids, vals, counts):
+    def _gather_entries(self, ids, vals, counts, packed32: bool = False):
         """All-gather every rank's frontier (ids int32, u64 values as int64)
-        as ONE padded (2, max count) int64 tensor per rank."""
+        as ONE padded int64 tensor per rank: 8-byte (id << 32 | value) words
+        when every value fits 32 bits (fixed-point mode), else (2, max count)
+        rows of ids and values."""
         torch = self.torch
         counts = [int(c) for c in counts]
         total = sum(counts)
@@ -245,14 +247,25 @@ class PartitionedDeltaStepping:
                     torch.empty(0, dtype=torch.int64, device=dev), 0)
         m = max(counts)
         mine = counts[self.pg.get_rank()]
-        buf = torch.zeros((2, m), dtype=torch.int64, device=self.xdev)
+        rows = 1 if packed32 else 2
+        buf = torch.zeros((rows, m), dtype=torch.int64, device=self.xdev)
         if mine:
-            buf[0, :mine] = ids.to(self.xdev).to(torch.int64)
-            buf[1, :mine] = vals.to(self.xdev)
+            i64 = ids.to(self.xdev).to(torch.int64)
+            v64 = vals.to(self.xdev)
+            if packed32:
+                buf[0, :mine] = (i64 << 32) | v64
+            else:
+                buf[0, :mine] = i64
+                buf[1, :mine] = v64
         outs = [torch.empty_like(buf) for _ in range(self.world)]
         self.pg.all_gather(outs, buf)
-        out_i = torch.cat([o[0, :k] for o, k in zip(outs, counts)]).to(torch.int32).to(dev)
-        out_v = torch.cat([o[1, :k] for o, k in zip(outs, counts)]).to(dev)
+        if packed32:
+            words = torch.cat([o[0, :k] for o, k in zip(outs, counts)])
+            out_i = (words >> 32).to(torch.int32).to(dev)
+            out_v = (words & 0xFFFFFFFF).to(dev)
+        else:
+            out_i = torch.cat([o[0, :k] for o, k in zip(outs, counts)]).to(torch.int32).to(dev)
+            out_v = torch.cat([o[1, :k] for o, k in zip(outs, counts)]).to(dev)
         return out_i, out_v, total
 
     # -- solve ---------------------------------------------------------
@@ -329,7 +342,7 @@ class PartitionedDeltaStepping:
                 idx = bucket_index_of(self._value(nm, mode, frac), delta)
                 continue
             visited += 1
-            F, Fv, nf = self._gather_entries(ids, vals, meta[:, 0])
+            F, Fv, nf = self._gather_entries(ids, vals, meta[:, 0], packed32=mode == MODE_FIXED32)
             exchanged += nf
             sh.s_add(F, Fv, nf)
             while True:  # light phases (sssp.py:292-301)
@@ -341,7 +354,7 @@ class PartitionedDeltaStepping:
                 meta = self._exchange_meta(ncnt, int(ovf))
                 if meta[:, 1].max():
                     return None
-                F, Fv, nf = self._gather_entries(nids, nvals, meta[:, 0])
+                F, Fv, nf = self._gather_entries(nids, nvals, meta[:, 0], packed32=mode == MODE_FIXED32)
                 exchanged += nf
                 if nf == 0:
                     break
