@@ -422,6 +422,7 @@ def partitioned_arm(args):
                   "counters_equal": (r0.outer_iterations, r0.inner_phases) == (want[1], want[2])}
     dist.barrier()
     torch.cuda.synchronize()
+    l0 = shard.launches()
     e0.record()
     m_local, phases, exch = 0, [], 0
     for k in range(args.steps):
@@ -439,6 +440,8 @@ def partitioned_arm(args):
     dist.all_reduce(m)
     t_ms = float(t.item())
     value = float(m.item()) / (t_ms * 1e-3) / 1e9
+    nl = torch.tensor([float(shard.launches() - l0)], dtype=torch.float64, device=xdev if shared else dev)
+    dist.all_reduce(nl)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -455,7 +458,7 @@ def partitioned_arm(args):
             "replicas": replicas,
             "e2e": None,
             "e2e_note": "inputs generated on each rank's device (no host copy exists at R-MAT 27)",
-            "gpu_launches": None,
+            "gpu_launches": int(nl.item()),
             "solver": {"phases_mean": statistics.mean(phases),
                        "frontier_entries_exchanged_per_source": exch / max(1, len(phases))},
         }), flush=True)

@@ -154,6 +154,11 @@ int ds_device_count(void);
  * 4 heavy relax.  Returns the number of steps written. */
 int64_t ds_debug_trace(ds_graph* g, uint64_t* out, int64_t cap);
 
+/* DS_TRACE=2 load-balance diagnostics of the last solve: out[0] = grid size,
+ * then for every step the time each CTA's warps finished it (steps x grid
+ * words).  Returns the number of words written after out[0]. */
+int64_t ds_debug_cta_times(ds_graph* g, uint64_t* out, int64_t cap);
+
 /* On-device synthetic R-MAT (Graph500 a,b,c,d = .57,.19,.19,.05; self-loops
  * dropped; symmetrised; deduplicated; fp32-lattice weight k*2^-24 per
  * undirected pair).  Bit-identical to paper_1911_06895_b200.graphs.rmat.
@@ -192,6 +197,8 @@ int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const uint64_t* v
                    uint64_t H, int32_t* out_ids, uint64_t* out_vals, int64_t* out_count,
                    int32_t* overflow);
 int ds_shard_result(ds_shard* s, double* out);
+/* Solver kernels this shard has launched so far (begin, scan, s_add, relax, result). */
+int64_t ds_shard_launches(const ds_shard* s);
 /* Shard [v0, v1) cut on the device from a resident graph handle. */
 int ds_shard_from_graph(ds_graph* g, int64_t v0, int64_t v1, ds_shard** out);
 

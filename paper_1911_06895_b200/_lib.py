@@ -28,6 +28,7 @@ EXPORTS = (
     "ds_last_error", "ds_device_count", "ds_gen_rmat", "ds_graph_download", "ds_debug_trace",
     "ds_shard_create", "ds_shard_destroy", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",
     "ds_shard_scan", "ds_shard_s_add", "ds_shard_relax", "ds_shard_result", "ds_shard_from_graph",
+    "ds_shard_launches", "ds_debug_cta_times",
     "ds_release_pool", "ds_ingest_parse", "ds_ingest_info", "ds_ingest_copy",
     "ds_ingest_error_line", "ds_ingest_free",
 )
@@ -141,6 +142,8 @@ def lib():
         L.ds_shard_relax.argtypes = [_vp, ctypes.c_int, _vp, _vp, _i64, u64, _vp, _vp,
                                      ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int32)]
         L.ds_shard_result.argtypes = [_vp, _vp]
+        L.ds_shard_launches.argtypes = [_vp]
+        L.ds_shard_launches.restype = _i64
         L.ds_shard_from_graph.argtypes = [_vp, _i64, _i64, ctypes.POINTER(_vp)]
         L.ds_shard_from_graph.restype = ctypes.c_int
         for name in ("ds_shard_create", "ds_shard_probe", "ds_shard_prepare", "ds_shard_begin",

@@ -41,6 +41,7 @@ int ds_internal_set_err(int code, const char* msg);
 
 struct ds_shard {
     int device = 0;
+    unsigned long long launches = 0;  // solver kernels launched (begin .. result)
     cudaStream_t stream = nullptr;
     long long n = 0, v0 = 0, nl = 0, nnz = 0;  // global n, owned range, local edges
     int nsm = 148;
@@ -441,9 +442,9 @@ extern "C" int ds_shard_begin(ds_shard* s, int64_t source) {
     cudaSetDevice(s->device);
     const long long sl = (source >= s->v0 && source < s->v0 + s->nl) ? source - s->v0 : -1;
     if (s->mode == DS_MODE_FIXED32)
-        k_shard_init<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>((unsigned*)s->dist, s->nl, sl);
+        (++s->launches), k_shard_init<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>((unsigned*)s->dist, s->nl, sl);
     else
-        k_shard_init<ModeF64><<<sgrid(s), kT, 0, s->stream>>>((unsigned long long*)s->dist, s->nl, sl);
+        (++s->launches), k_shard_init<ModeF64><<<sgrid(s), kT, 0, s->stream>>>((unsigned long long*)s->dist, s->nl, sl);
     SCK(cudaGetLastError());
     SCK(cudaMemsetAsync(s->fbits, 0, sizeof(unsigned) * (std::max<long long>(s->nl, 1LL) / 32 + 1), s->stream));
     SCK(cudaMemsetAsync(s->sbits, 0, sizeof(unsigned) * (s->n / 32 + 1), s->stream));
@@ -463,11 +464,11 @@ extern "C" int ds_shard_scan(ds_shard* s, uint64_t L, uint64_t H, int32_t* out_i
     SCK(cudaMemcpyAsync(s->counters, init, sizeof(init), cudaMemcpyHostToDevice, s->stream));
     if (s->nl) {
         if (s->mode == DS_MODE_FIXED32)
-            k_shard_scan<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>(
+            (++s->launches), k_shard_scan<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>(
                 (const unsigned*)s->dist, s->nl, s->v0, (unsigned)L, (unsigned)H, out_ids,
                 (unsigned long long*)out_vals, s->counters);
         else
-            k_shard_scan<ModeF64><<<sgrid(s), kT, 0, s->stream>>>(
+            (++s->launches), k_shard_scan<ModeF64><<<sgrid(s), kT, 0, s->stream>>>(
                 (const unsigned long long*)s->dist, s->nl, s->v0, L, H, out_ids,
                 (unsigned long long*)out_vals, s->counters);
     }
@@ -487,7 +488,7 @@ extern "C" int ds_shard_s_add(ds_shard* s, const int32_t* ids, const uint64_t* v
     unsigned long long c2 = (unsigned long long)s->scount;
     SCK(cudaMemcpyAsync(s->counters + 2, &c2, sizeof(c2), cudaMemcpyHostToDevice, s->stream));
     if (count > 0)
-        k_shard_s_add<<<sgrid(s), kT, 0, s->stream>>>(ids, (const unsigned long long*)vals, count,
+        (++s->launches), k_shard_s_add<<<sgrid(s), kT, 0, s->stream>>>(ids, (const unsigned long long*)vals, count,
                                                        s->sbits, s->sval, s->slist, s->counters);
     SCK(cudaGetLastError());
     SCK(cudaMemcpyAsync(&c2, s->counters + 2, sizeof(c2), cudaMemcpyDeviceToHost, s->stream));
@@ -510,7 +511,7 @@ static int shard_push(ds_shard* s, bool light, const int* ids, const unsigned lo
     p.chunk_start = s->chunk_start;
     SCK(cudaMemsetAsync(s->slot, 0, sizeof(StepSlot), s->stream));
     const unsigned grid = (unsigned)(s->nsm * 4);
-    k_shard_capture<M><<<grid, kThreads, 0, s->stream>>>(p, s->slot, ids, vals, count,
+    (++s->launches), k_shard_capture<M><<<grid, kThreads, 0, s->stream>>>(p, s->slot, ids, vals, count,
                                                          light ? s->Lptr : s->Hptr);
     SCK(cudaGetLastError());
     StepSlot h{};
@@ -528,10 +529,10 @@ static int shard_push(ds_shard* s, bool light, const int* ids, const unsigned lo
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_shard_relax<M, false>, kThreads, smem);
     const unsigned rgrid = (unsigned)(s->nsm * std::max(occ, 1));
     if (light)
-        k_shard_relax<M, true><<<rgrid, kThreads, smem, s->stream>>>(
+        (++s->launches), k_shard_relax<M, true><<<rgrid, kThreads, smem, s->stream>>>(
             p, s->slot, E, Rc, (const typename M::Edge*)s->Ledges, H, s->tmp_ids, s->fbits);
     else
-        k_shard_relax<M, false><<<rgrid, kThreads, smem, s->stream>>>(
+        (++s->launches), k_shard_relax<M, false><<<rgrid, kThreads, smem, s->stream>>>(
             p, s->slot, E, Rc, (const typename M::Edge*)s->Hedges, H, nullptr, nullptr);
     SCK(cudaGetLastError());
     SCK(cudaMemcpyAsync(&h, s->slot, sizeof(StepSlot), cudaMemcpyDeviceToHost, s->stream));
@@ -557,12 +558,12 @@ extern "C" int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const 
         const long long sc = s->scount;
         if (sc > 0) {
             unsigned long long* sv = (unsigned long long*)s->cnt_scratch;
-            k_shard_gather_s<<<sgrid(s), kT, 0, s->stream>>>(s->slist, sc, s->sval, sv);
+            (++s->launches), k_shard_gather_s<<<sgrid(s), kT, 0, s->stream>>>(s->slist, sc, s->sval, sv);
             SCK(cudaGetLastError());
             rc = fx ? shard_push<ModeFixed>(s, false, s->slist, sv, sc, 0u, &nf, &ovf)
                     : shard_push<ModeF64>(s, false, s->slist, sv, sc, 0ull, &nf, &ovf);
             if (rc) return rc;
-            k_shard_s_clear<<<sgrid(s), kT, 0, s->stream>>>(s->slist, sc, s->sbits);
+            (++s->launches), k_shard_s_clear<<<sgrid(s), kT, 0, s->stream>>>(s->slist, sc, s->sbits);
             SCK(cudaGetLastError());
             SCK(cudaStreamSynchronize(s->stream));
         }
@@ -580,11 +581,11 @@ extern "C" int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const 
     }
     if (nf > 0) {
         if (fx)
-            k_shard_emit<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>(s->tmp_ids, nf, (const unsigned*)s->dist,
+            (++s->launches), k_shard_emit<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>(s->tmp_ids, nf, (const unsigned*)s->dist,
                                                                    s->v0, s->fbits, out_ids,
                                                                    (unsigned long long*)out_vals);
         else
-            k_shard_emit<ModeF64><<<sgrid(s), kT, 0, s->stream>>>(
+            (++s->launches), k_shard_emit<ModeF64><<<sgrid(s), kT, 0, s->stream>>>(
                 s->tmp_ids, nf, (const unsigned long long*)s->dist, s->v0, s->fbits, out_ids,
                 (unsigned long long*)out_vals);
         SCK(cudaGetLastError());
@@ -596,6 +597,8 @@ extern "C" int ds_shard_relax(ds_shard* s, int heavy, const int32_t* ids, const 
 }
 
 // Owned distances as float64 (+inf = unreachable), out holds nl doubles.
+extern "C" int64_t ds_shard_launches(const ds_shard* s) { return s ? (int64_t)s->launches : 0; }
+
 extern "C" int ds_shard_result(ds_shard* s, double* out) {
     if (!s) return ds_internal_set_err(DS_EINVAL, "null shard");
     cudaSetDevice(s->device);
@@ -603,10 +606,10 @@ extern "C" int ds_shard_result(ds_shard* s, double* out) {
         double* d = nullptr;
         SCK(cudaMalloc(&d, sizeof(double) * s->nl));
         if (s->mode == DS_MODE_FIXED32)
-            k_shard_result<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>((const unsigned*)s->dist, s->nl,
+            (++s->launches), k_shard_result<ModeFixed><<<sgrid(s), kT, 0, s->stream>>>((const unsigned*)s->dist, s->nl,
                                                                       s->frac, d);
         else
-            k_shard_result<ModeF64><<<sgrid(s), kT, 0, s->stream>>>((const unsigned long long*)s->dist,
+            (++s->launches), k_shard_result<ModeF64><<<sgrid(s), kT, 0, s->stream>>>((const unsigned long long*)s->dist,
                                                                     s->nl, 0, d);
         SCK(cudaGetLastError());
         SCK(cudaMemcpyAsync(out, d, sizeof(double) * s->nl, cudaMemcpyDefault, s->stream));

@@ -177,6 +177,10 @@ class DeviceShard:
                                              ctypes.byref(oc), ctypes.byref(ov)))
         return bool(ov.value)
 
+    def launches(self) -> int:
+        """Solver kernels this shard has launched so far."""
+        return int(_lib.lib().ds_shard_launches(self._h))
+
     def result(self, on_device: bool = False):
         """Owned float64 distances: numpy (host) or a torch tensor left on the GPU."""
         if on_device:
