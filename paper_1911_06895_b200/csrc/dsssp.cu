@@ -191,6 +191,13 @@ struct SolveCtx {
     double* out2 = nullptr;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t copied[2] = {nullptr, nullptr};
+    // pipelined batches: a second control block / event pair so the next
+    // source's kernel is queued before the host reads this one's results
+    Ctl* ctl2 = nullptr;
+    Ctl* h_ctl2 = nullptr;
+    cudaEvent_t ev0b = nullptr, ev1b = nullptr;
+    cudaEvent_t done = nullptr, done2 = nullptr;  // control block copied to the host
+    bool pending = false;                          // launched, not finished (async mode)
 };
 
 struct ds_graph {
@@ -258,6 +265,9 @@ struct ds_graph {
     long long n_active = 0;
     Ctl* ctl = nullptr;
     Ctl* h_ctl = nullptr;  // host mirror
+    Ctl* ctl2 = nullptr;   // pipelined batches: context 0's second control block
+    Ctl* h_ctl2 = nullptr;
+    cudaEvent_t ev0b = nullptr, ev1b = nullptr, done = nullptr, done2 = nullptr;
     PrepStats* pstat = nullptr;
     PrepStats* h_pstat = nullptr;
     double* out = nullptr;
@@ -315,6 +325,12 @@ static SolveCtx main_ctx(ds_graph* g) {
     x.out2 = g->out2;
     x.copy_stream = g->copy_stream;
     x.copied[0] = g->copied[0];
+    x.ctl2 = g->ctl2;
+    x.h_ctl2 = g->h_ctl2;
+    x.ev0b = g->ev0b;
+    x.ev1b = g->ev1b;
+    x.done = g->done;
+    x.done2 = g->done2;
     x.copied[1] = g->copied[1];
     return x;
 }
@@ -329,6 +345,10 @@ static void free_all(ds_graph* g) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (SolveCtx* x : g->extra) {
+        for (cudaEvent_t e : {x->ev0b, x->ev1b, x->done, x->done2})
+            if (e) cudaEventDestroy(e);
+        delete x->h_ctl2;
+        if (x->ctl2) cudaFree(x->ctl2);
         void* q[] = {x->dist, x->fbits, x->sbits, x->F0, x->F1, x->S0, x->S1, x->Fv0, x->Fv1,
                      x->req, x->Rpre, x->Rbase, x->Rd, x->chunk_start, x->ctl, x->out, x->out2, x->csum};
         for (void* p : q)
@@ -1522,8 +1542,14 @@ static auto lex_kernel() {
         return sssp_persistent_kernel<M, false>;
 }
 
+static int finish_solve(ds_graph* g, SolveCtx& x, int* dev_status);
+
+// mode 0: launch and finish (synchronous); 1: launch only (no giant-push
+// handoff), the control block lands in x.h_ctl when x.done fires; then
+// finish_solve() completes it.
 template <class M>
-static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned grid, int* dev_status) {
+static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned grid, int* dev_status,
+                        int mode = 0) {
     KParams<M> p{};
     p.n = g->n;
     p.source = source;
@@ -1594,7 +1620,7 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         p.lex = g->lex ? 1 : 0;
         p.ksub_log2 = __builtin_ctz((unsigned)g->ksub);
         p.WD = g->WD;
-        if (g->lex) p.big_light = p.big_heavy = ~0ull;  // no giant-push handoff (state not resumable)
+        if (g->lex || mode == 1) p.big_light = p.big_heavy = ~0ull;  // no giant-push handoff
         if (getenv("DS_DEBUG_PREP"))
             fprintf(stderr, "[ds] launch: lex=%d ksub=%d WD=%u nL=%lld nH=%lld refL=%lld mode=%d small=%d\n",
                     p.lex, g->ksub, p.WD, g->nL, g->nH, g->refL, g->mode, (int)g->small);
@@ -1681,6 +1707,11 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         // kernel_ms excludes the host's wake-up after the synchronize below
         CK(cudaEventRecord(x.ev1, x.stream));
         CK(cudaMemcpyAsync(x.h_ctl, x.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, x.stream));
+        if (mode == 1) {
+            CK(cudaEventRecord(x.done, x.stream));
+            x.pending = true;
+            return DS_OK;
+        }
         CK(cudaStreamSynchronize(x.stream));
         const Ctl& h = *x.h_ctl;
         if (h.abort || h.status != 0 || h.rs_req == 0) break;
@@ -1698,13 +1729,22 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         }
         CK(cudaGetLastError());
     }
-    const Ctl& c = *x.h_ctl;
-    // an interrupted solve may leave dedup bits set: clear them for the next one
-    if (c.abort || c.status != 0) {
-        CK(cudaMemsetAsync(x.fbits, 0, 2 * sizeof(unsigned) * g->nwords, x.stream));
-        CK(cudaMemsetAsync(x.sbits, 0, sizeof(unsigned) * g->nwords, x.stream));
-        CK(cudaStreamSynchronize(x.stream));
+    (void)p;
+    return finish_solve(g, x, dev_status);
+}
+
+// Status, trace and counters of a launched solve (after its control block
+// reached the host).  Dedup bitmaps left set by an interrupted solve need no
+// host clean-up: every launch clears them in its init phase.
+static int finish_solve(ds_graph* g, SolveCtx& x, int* dev_status) {
+    if (x.pending) {
+        CK(cudaEventSynchronize(x.done));
+        x.pending = false;
     }
+    unsigned long long* trace = x.traced ? g->trace : nullptr;
+    double tmo = 0.0;
+    if (const char* e = getenv("DS_TIMEOUT_S")) tmo = atof(e);
+    const Ctl& c = *x.h_ctl;
     if (c.abort) {
         if (trace) {  // keep the partial timeline for post-mortems
             g->trace_len = g->trace_cap;
@@ -1725,6 +1765,9 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
                         (double)(c.t_exit - last[0]) / 1e3);
         }
     }
+    if (c.cnt_atomics && getenv("DS_DEBUG_PREP"))
+        fprintf(stderr, "[ds] light atomics %llu, improving %llu, edges scanned %llu\n", c.cnt_atomics,
+                c.cnt_improved, c.edges_scanned);
     *dev_status = c.status;
     if (c.status == 0 && c.lexsat) *dev_status = kDevLexFail;
     return DS_OK;
@@ -1832,6 +1875,12 @@ static int make_ctx(ds_graph* g, SolveCtx** out) {
     CK(cudaMalloc(&x->csum, sizeof(unsigned long long) * (n / (32 * kRangePer) + 2)));
     CK(cudaMalloc(&x->ctl, sizeof(Ctl)));
     x->h_ctl = new Ctl();
+    CK(cudaMalloc(&x->ctl2, sizeof(Ctl)));
+    x->h_ctl2 = new Ctl();
+    CK(cudaEventCreate(&x->ev0b));
+    CK(cudaEventCreate(&x->ev1b));
+    CK(cudaEventCreateWithFlags(&x->done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&x->done2, cudaEventDisableTiming));
     CK(cudaMalloc(&x->out, sizeof(double) * n));
     CK(cudaMemsetAsync(x->fbits, 0, 2 * sizeof(unsigned) * g->nwords, x->stream));
     CK(cudaMemsetAsync(x->sbits, 0, sizeof(unsigned) * g->nwords, x->stream));
@@ -1889,8 +1938,17 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
             if ((rc = streaming(&x->out2, &x->copy_stream, x->copied))) return rc;
         }
     }
+    if (!g->ctl2) {  // context 0's pipelining resources (the extra contexts own theirs)
+        CK(cudaMalloc(&g->ctl2, sizeof(Ctl)));
+        g->h_ctl2 = new Ctl();
+        CK(cudaEventCreate(&g->ev0b));
+        CK(cudaEventCreate(&g->ev1b));
+        CK(cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&g->done2, cudaEventDisableTiming));
+    }
     std::vector<SolveCtx> ctx;
     ctx.push_back(main_ctx(g));
+    ctx[0].traced = false;  // pipelined launches would race on the one trace buffer
     for (int t = 1; t < T; ++t) ctx.push_back(*g->extra[t - 1]);
     if (T > 1) {
         // every context on its own non-blocking stream (the handle's stream
@@ -1912,26 +1970,28 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
         cudaSetDevice(g->device);
         SolveCtx& x = ctx[t];
         double* const outs[2] = {x.out, x.out2};
-        for (long long j = 0;; ++j) {
-            const long long i = next.fetch_add(1);
-            if (i >= k) break;
-            const int b = (int)(j & 1);
-            if (dist_out) {
-                // alternate output buffers; reuse one only after its D2H finished
-                x.out = outs[b];
-                if (j >= 2 && cudaStreamWaitEvent(x.stream, x.copied[b], 0) != cudaSuccess) {
-                    err[t] = set_err(DS_ECUDA, "CUDA error ordering a batch output buffer");
-                    msg[t] = g_err;
-                    next.store(k);
-                    break;
-                }
-            }
+        // Pipelined: source j+1's kernel is queued on the stream before the
+        // host waits for source j's control block, so consecutive solves of a
+        // context run back to back on the GPU.  Two views of the context
+        // alternate the control block and timing events.
+        SolveCtx xv[2] = {x, x};
+        xv[1].ctl = x.ctl2;
+        xv[1].h_ctl = x.h_ctl2;
+        xv[1].ev0 = x.ev0b;
+        xv[1].ev1 = x.ev1b;
+        xv[1].done = x.done2;
+        struct Pending {
+            long long i;
+            int v;
+            bool on;
+        } pend = {0, 0, false};
+        auto finish = [&](const Pending& q) -> int {
             int st = 0;
-            int r = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, x, sources[i], grid, &st)
-                                               : launch_solve<ModeF64>(g, x, sources[i], grid, &st);
+            SolveCtx& y = xv[q.v];
+            int r = finish_solve(g, y, &st);
             if (r == DS_OK && (st == kDevOverflow || st == kDevLexFail)) {
-                redo[t].push_back({i, st});  // rerun (binary64 / reference schedule) after the batch
-                continue;
+                redo[t].push_back({q.i, st});  // rerun (binary64 / reference schedule) after the batch
+                return DS_OK;
             }
             if (r == DS_OK && st == DS_ENOCONVERGE)
                 r = set_err(DS_ENOCONVERGE,
@@ -1939,21 +1999,50 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
                             g->ceiling);
             else if (r == DS_OK && st != 0)
                 r = set_err(DS_ECUDA, "device solver status %d", st);
-            if (r == DS_OK && stats) fill_stats(g, x, delta, flags, 0, stats + i);
+            if (r == DS_OK && stats) fill_stats(g, y, delta, flags, 0, stats + q.i);
             if (r == DS_OK && dist_out) {
-                // launch_solve returned after its stream drained: the copy
-                // needs no event and overlaps the next source's solve
-                cudaError_t e = cudaMemcpyAsync(dist_out + i * n, x.out, sizeof(double) * n,
-                                                cudaMemcpyDefault, x.copy_stream);
-                if (e == cudaSuccess) e = cudaEventRecord(x.copied[b], x.copy_stream);
+                // the copy waits for this source's kernel and overlaps the next one
+                cudaError_t e = cudaStreamWaitEvent(x.copy_stream, y.ev1, 0);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(dist_out + q.i * n, y.out, sizeof(double) * n, cudaMemcpyDefault,
+                                        x.copy_stream);
+                if (e == cudaSuccess) e = cudaEventRecord(x.copied[q.v], x.copy_stream);
                 if (e != cudaSuccess)
                     r = set_err(DS_ECUDA, "CUDA error %s copying batch result", cudaGetErrorName(e));
             }
+            return r;
+        };
+        for (long long j = 0;; ++j) {
+            const long long i = next.fetch_add(1);
+            if (i >= k) break;
+            const int v = (int)(j & 1);
+            if (dist_out) {
+                // alternate output buffers; reuse one only after its D2H finished
+                xv[v].out = outs[v];
+                if (j >= 2 && cudaStreamWaitEvent(x.stream, x.copied[v], 0) != cudaSuccess) {
+                    err[t] = set_err(DS_ECUDA, "CUDA error ordering a batch output buffer");
+                    msg[t] = g_err;
+                    next.store(k);
+                    break;
+                }
+            }
+            int st = 0;
+            int r = g->mode == DS_MODE_FIXED32 ? launch_solve<ModeFixed>(g, xv[v], sources[i], grid, &st, 1)
+                                               : launch_solve<ModeF64>(g, xv[v], sources[i], grid, &st, 1);
+            if (r == DS_OK && pend.on) r = finish(pend);
+            pend = {i, v, true};
             if (r != DS_OK) {
                 err[t] = r;
                 msg[t] = g_err;
                 next.store(k);  // stop the other workers after their current source
                 break;
+            }
+        }
+        if (pend.on && err[t] == DS_OK) {
+            const int r = finish(pend);
+            if (r != DS_OK) {
+                err[t] = r;
+                msg[t] = g_err;
             }
         }
         if (dist_out && cudaStreamSynchronize(x.copy_stream) != cudaSuccess && err[t] == DS_OK) {

@@ -264,6 +264,12 @@ constexpr bool kCsum = DS_CSUM && !(DS_PULL_LIGHT || DS_PULL_HEAVY);
 #ifndef DS_PIPE
 #define DS_PIPE 0  // software-pipelined push: next chunk's entries load under this chunk's edges
 #endif
+#ifndef DS_PRECHECK_CUT
+#define DS_PRECHECK_CUT 32768  // > 0: only pre-check reads of solver ids below it go through L1 (measured -2%)
+#endif
+#ifndef DS_COUNT
+#define DS_COUNT 0  // count the light push atomics (diagnostics build)
+#endif
 #ifndef DS_L2PF
 #define DS_L2PF 0  // bulk L2 prefetch of the next chunk's edges (measured slower: 5.34 -> 5.40 ms)
 #endif
@@ -290,6 +296,7 @@ struct Ctl {
     unsigned long long phases, visited, edges_scanned, barriers, steps;
     long long last_bucket;
     unsigned long long pulls;  // light/heavy steps run as pulls
+    unsigned long long cnt_atomics, cnt_improved;  // DS_COUNT=1 builds: light atomics issued / improving
     // resumable solver: the persistent kernel hands a giant push to a
     // standalone launch (k_big_relax) and is relaunched where it left off
     unsigned long long rs_pos, rs_req, rs_E, rs_Rc;
@@ -1204,8 +1211,14 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                     // a stale (L1) value is >= the current one: it can only
                     // cause a redundant atomic, never a missed improvement
                     const unsigned v = M::col(ed[j]);
+#if DS_PRECHECK_CUT
+                    // hub targets (solver ids below the cut) through L1, the rest
+                    // straight from L2 so they do not evict the hub lines
+                    cur[j] = v < (unsigned)DS_PRECHECK_CUT ? p.dist[v] : __ldcg(p.dist + v);
+#else
                     cur[j] = (LIGHT || !kHeavyRed) ? (DS_PRECHECK_L1 ? p.dist[v] : __ldcg(p.dist + v))
                                                    : M::INF;
+#endif
                 } else {
                     overflow = true;
                 }
@@ -1221,6 +1234,22 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                 old[j] = nd[j];
                 if (32 * j < left && nd[j] < cur[j]) old[j] = atomicMin(p.dist + M::col(ed[j]), nd[j]);
             }
+#if DS_COUNT
+            {
+                unsigned long long na = 0, ni = 0;
+#pragma unroll
+                for (int j = 0; j < kRelPer; ++j) {
+                    if (32 * j < left && nd[j] < cur[j]) ++na;
+                    if (32 * j < left && nd[j] < old[j]) ++ni;
+                }
+                na = warp_sum(na);
+                ni = warp_sum(ni);
+                if (lane == 0) {
+                    atomicAdd(&p.ctl->cnt_atomics, na);
+                    atomicAdd(&p.ctl->cnt_improved, ni);
+                }
+            }
+#endif
 #if DS_DEFER_APPEND
 #pragma unroll
             for (int j = 0; j < kRelPer; ++j) {
@@ -1515,6 +1544,14 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         const long long stride = (long long)gridDim.x * kThreads;
         for (long long v = (long long)blockIdx.x * kThreads + threadIdx.x; v < n_scan; v += stride)
             p.dist[v] = (v == src) ? (D)0 : M::INF;
+        // dedup bitmaps start clear: a previous solve on these buffers may
+        // have stopped mid-bucket (overflow / rerun), and pipelined batches
+        // queue this launch before the host has seen that solve's status
+        for (long long k = (long long)blockIdx.x * kThreads + threadIdx.x; k < (n_scan + 31) / 32; k += stride) {
+            p.fbits[0][k] = 0u;
+            p.fbits[1][k] = 0u;
+            p.sbits[k] = 0u;
+        }
         if (kSum) {
             const long long per = 32ll * kRangePer;
             for (long long k = (long long)blockIdx.x * kThreads + threadIdx.x; k < (n_scan + per - 1) / per;
