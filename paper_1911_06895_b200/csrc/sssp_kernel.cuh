@@ -878,6 +878,38 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
     }
 }
 
+// UNSETTLED capture for the heavy gather (dense: most rows of the active
+// prefix are unsettled at a giant bucket): CTA-uniform rounds of 32 x kUnsetPer
+// consecutive rows per warp (coalesced dist / offset reads), one entry
+// reservation per CTA round.  Entries carry the row id; rows >= n_scan and
+// rows without heavy edges get none.
+constexpr int kUnsetPer = 4;
+template <class M>
+__device__ void capture_unsettled(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
+                                  typename M::D T, unsigned long long n_scan) {
+    using D = typename M::D;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const unsigned long long per_warp = 32ull * kUnsetPer;
+    const unsigned long long nblk = (n_scan + per_warp - 1) / per_warp;
+    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    for (unsigned long long cbase = (unsigned long long)blockIdx.x * kWarps; cbase < nblk; cbase += nw) {
+        const unsigned long long c = cbase + wib;
+        D cd[kUnsetPer];
+        long long off[kUnsetPer], deg[kUnsetPer];
+#pragma unroll
+        for (int j = 0; j < kUnsetPer; ++j) {
+            const unsigned long long v = c * per_warp + lane + 32ull * j;
+            const bool in = c < nblk && v < n_scan;
+            const D d = in ? __ldcg(p.dist + v) : (D)0;
+            const bool un = in && d >= T;
+            cd[j] = (D)v;
+            off[j] = un ? __ldg(p.Hptr + v) : 0;
+            deg[j] = un ? __ldg(p.Hptr + v + 1) - off[j] : 0;
+        }
+        capture_emit_cta<M, kUnsetPer>(p, sm, slot, lane, wib, cd, off, deg);
+    }
+}
+
 // LIST capture: a frontier / S list.  Snapshots d after the barrier that
 // ended the previous phase (VALS: the list carries values produced by a pull
 // and this step commits them to t first), looks up degrees in `ptr`, clears
@@ -1968,8 +2000,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 }
                 if ((double)E > (double)p.hpull_ratio * (double)U &&
                     M::heavy_beyond(Lw, Hw, lo, hi, p.min_heavy)) {
-                    capture_range<M, false, true>(p, sm, &c->slot[st % 3], H, M::INF, nullptr, nullptr,
-                                                  (unsigned long long)n_scan, nullptr, 0ull, p.Hptr);
+                    capture_unsettled<M>(p, sm, &c->slot[st % 3], H, (unsigned long long)n_scan);
                     if (!end_step(11, (unsigned long long)n_scan)) return;
                     const unsigned long long pre = ldcg(&prev()->re_packed);
                     const unsigned long long Ep = pre & kMask33;
