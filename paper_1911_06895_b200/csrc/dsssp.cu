@@ -43,6 +43,48 @@ using namespace ds;
 #include <unordered_map>
 
 namespace {
+// Host mirrors of the control blocks live in pinned memory: a D2H copy into
+// pageable memory returns only after the copy (and so the kernel queued
+// before it) finished, which serialised the pipelined batch launches.  The
+// slabs are allocated once per process and recycled (cudaFreeHost costs ms).
+struct PinnedCtlPool {
+    std::mutex m;
+    std::vector<Ctl*> free_;
+};
+PinnedCtlPool& pinned_ctl_pool() {
+    static PinnedCtlPool* p = new PinnedCtlPool();  // never destroyed
+    return *p;
+}
+Ctl* host_ctl_alloc() {
+    PinnedCtlPool& P = pinned_ctl_pool();
+    std::lock_guard<std::mutex> lk(P.m);
+    if (P.free_.empty()) {
+        constexpr int kSlab = 16;
+        Ctl* slab = nullptr;
+        if (cudaHostAlloc((void**)&slab, sizeof(Ctl) * kSlab, cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return new Ctl();  // pageable fallback (correct, not pipelined)
+        }
+        for (int i = 0; i < kSlab; ++i) P.free_.push_back(slab + i);
+    }
+    Ctl* c = P.free_.back();
+    P.free_.pop_back();
+    memset((void*)c, 0, sizeof(Ctl));
+    return c;
+}
+void host_ctl_free(Ctl* c) {
+    if (!c) return;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, c) != cudaSuccess || a.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        delete c;
+        return;
+    }
+    PinnedCtlPool& P = pinned_ctl_pool();
+    std::lock_guard<std::mutex> lk(P.m);
+    P.free_.push_back(c);
+}
+
 struct BufferPool {
     std::mutex m;
     std::multimap<std::pair<int, size_t>, void*> free_;
@@ -347,7 +389,7 @@ static void free_all(ds_graph* g) {
     for (SolveCtx* x : g->extra) {
         for (cudaEvent_t e : {x->ev0b, x->ev1b, x->done, x->done2})
             if (e) cudaEventDestroy(e);
-        delete x->h_ctl2;
+        host_ctl_free(x->h_ctl2);
         if (x->ctl2) cudaFree(x->ctl2);
         void* q[] = {x->dist, x->fbits, x->sbits, x->F0, x->F1, x->S0, x->S1, x->Fv0, x->Fv1,
                      x->req, x->Rpre, x->Rbase, x->Rd, x->chunk_start, x->ctl, x->out, x->out2, x->csum};
@@ -356,7 +398,7 @@ static void free_all(ds_graph* g) {
         for (cudaEvent_t e : x->copied)
             if (e) cudaEventDestroy(e);
         if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
-        delete x->h_ctl;
+        host_ctl_free(x->h_ctl);
         if (x->ev0) cudaEventDestroy(x->ev0);
         if (x->ev1) cudaEventDestroy(x->ev1);
         if (x->ready) cudaEventDestroy(x->ready);
@@ -370,7 +412,11 @@ static void free_all(ds_graph* g) {
         if (e) cudaEventDestroy(e);
     if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
     if (g->batch_stream) cudaStreamDestroy(g->batch_stream);
-    delete g->h_ctl;  // small pageable mirrors (cudaFreeHost costs ms per call)
+    host_ctl_free(g->h_ctl);  // pinned mirrors return to the process pool
+    host_ctl_free(g->h_ctl2);
+    if (g->ctl2) cudaFree(g->ctl2);
+    for (cudaEvent_t e : {g->ev0b, g->ev1b, g->done, g->done2})
+        if (e) cudaEventDestroy(e);
     delete g->h_pstat;
     if (g->ev0) cudaEventDestroy(g->ev0);
     if (g->ev1) cudaEventDestroy(g->ev1);
@@ -879,7 +925,7 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaMalloc(&g->chunk_start, sizeof(unsigned) * (g->nnz / kChunk + 4)));
     CK(cudaMalloc(&g->csum, sizeof(unsigned long long) * (n / (32 * kRangePer) + 2)));
     CK(cudaMalloc(&g->ctl, sizeof(Ctl)));
-    g->h_ctl = new Ctl();
+    g->h_ctl = host_ctl_alloc();
     CK(cudaMalloc(&g->pstat, sizeof(PrepStats)));
     g->h_pstat = new PrepStats();
     CK(cudaMalloc(&g->out, sizeof(double) * n));
@@ -1874,9 +1920,9 @@ static int make_ctx(ds_graph* g, SolveCtx** out) {
     CK(cudaMalloc(&x->chunk_start, sizeof(unsigned) * (g->nnz / kChunk + 4)));
     CK(cudaMalloc(&x->csum, sizeof(unsigned long long) * (n / (32 * kRangePer) + 2)));
     CK(cudaMalloc(&x->ctl, sizeof(Ctl)));
-    x->h_ctl = new Ctl();
+    x->h_ctl = host_ctl_alloc();
     CK(cudaMalloc(&x->ctl2, sizeof(Ctl)));
-    x->h_ctl2 = new Ctl();
+    x->h_ctl2 = host_ctl_alloc();
     CK(cudaEventCreate(&x->ev0b));
     CK(cudaEventCreate(&x->ev1b));
     CK(cudaEventCreateWithFlags(&x->done, cudaEventDisableTiming));
@@ -1940,7 +1986,7 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
     }
     if (!g->ctl2) {  // context 0's pipelining resources (the extra contexts own theirs)
         CK(cudaMalloc(&g->ctl2, sizeof(Ctl)));
-        g->h_ctl2 = new Ctl();
+        g->h_ctl2 = host_ctl_alloc();
         CK(cudaEventCreate(&g->ev0b));
         CK(cudaEventCreate(&g->ev1b));
         CK(cudaEventCreateWithFlags(&g->done, cudaEventDisableTiming));
