@@ -270,6 +270,8 @@ struct ds_graph {
     double lexfail_delta = NAN;   // delta whose lex-mode keys went out of range
     long long* Lptr = nullptr;
     long long* Hptr = nullptr;
+    uint2* Linfo = nullptr;  // per row {offset mod 2^32, degree} of A_L / A_H (the captures' one-load form)
+    uint2* Hinfo = nullptr;
     void* Ledges = nullptr;
     void* Hedges = nullptr;
     size_t Lcap = 0, Hcap = 0;
@@ -379,6 +381,7 @@ static SolveCtx main_ctx(ds_graph* g) {
 
 static void free_all(ds_graph* g) {
     void* ptrs[] = {g->indptr, g->col,  g->w,     g->Lptr,  g->Hptr,       g->Ledges, g->Hedges,
+                    g->Linfo,  g->Hinfo,
                     g->dist,   g->fbits, g->sbits, g->F0,  g->F1,  g->Fv0, g->Fv1, g->S0, g->S1, g->req, g->Rpre,
                     g->planL.rowid, g->planL.cptr, g->planL.chunk_row, g->planL.span,
                     g->planH.rowid, g->planH.cptr, g->planH.chunk_row, g->planH.span,
@@ -794,6 +797,17 @@ __global__ void k_symmetry_sums(const long long* indptr, const int* col, const d
     }
 }
 
+// {offset mod 2^32, degree} per row from the light / heavy row offsets
+__global__ void k_row_info(const long long* Lptr, const long long* Hptr, long long n, uint2* Linfo,
+                           uint2* Hinfo) {
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
+         r += (long long)gridDim.x * blockDim.x) {
+        const long long l0 = Lptr[r], l1 = Lptr[r + 1], h0 = Hptr[r], h1 = Hptr[r + 1];
+        Linfo[r] = make_uint2((unsigned)l0, (unsigned)(l1 - l0));
+        Hinfo[r] = make_uint2((unsigned)h0, (unsigned)(h1 - h0));
+    }
+}
+
 template <class D>
 __global__ void k_fill(D* a, long long m, D v) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
@@ -931,6 +945,8 @@ static int alloc_scratch(ds_graph* g) {
     CK(cudaMalloc(&g->out, sizeof(double) * n));
     CK(cudaMalloc(&g->Lptr, sizeof(long long) * (n + 1)));
     CK(cudaMalloc(&g->Hptr, sizeof(long long) * (n + 1)));
+    CK(cudaMalloc(&g->Linfo, sizeof(uint2) * n));
+    CK(cudaMalloc(&g->Hinfo, sizeof(uint2) * n));
     CK(cudaMemsetAsync(g->fbits, 0, 2 * sizeof(unsigned) * g->nwords, g->stream));
     CK(cudaMemsetAsync(g->sbits, 0, sizeof(unsigned) * g->nwords, g->stream));
     CK(cudaEventCreate(&g->ev0));
@@ -1490,6 +1506,8 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     if (g->nL >= (1LL << 32) || g->nH >= (1LL << 32))
         return set_err(DS_EINVAL, "light or heavy edge count %lld exceeds 2^32",
                        std::max(g->nL, g->nH));
+    k_row_info<<<grid, 256, 0, g->stream>>>(g->Lptr, g->Hptr, n, g->Linfo, g->Hinfo);
+    CK(cudaGetLastError());
     const size_t esz = mode == DS_MODE_FIXED32 ? sizeof(uint2) : sizeof(EdgeF64);
     if ((rc = ensure_edges(&g->Ledges, &g->Lcap, esz * (size_t)g->nL))) return rc;
     if ((rc = ensure_edges(&g->Hedges, &g->Hcap, esz * (size_t)g->nH))) return rc;
@@ -1614,6 +1632,8 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     p.Ledges = (const typename M::Edge*)g->Ledges;
     p.Hptr = g->Hptr;
     p.Hedges = (const typename M::Edge*)g->Hedges;
+    p.Linfo = g->Linfo;
+    p.Hinfo = g->Hinfo;
     p.dist = (typename M::D*)x.dist;
     p.fbits[0] = x.fbits;
     p.fbits[1] = x.fbits + g->nwords;

@@ -212,6 +212,10 @@ constexpr int kCapPer = DS_CAP_PER;  // capture (list): entries per lane per rou
 #ifndef DS_QUEUE
 #define DS_QUEUE 256
 #endif
+#ifndef DS_BULK_CLEAR
+#define DS_BULK_CLEAR 16384  // frontier lists at least this long clear the dedup bitmap as a whole
+#endif
+constexpr unsigned long long kBulkClearMin = DS_BULK_CLEAR;
 constexpr int kRangePer = 16;     // capture (range): vertices per lane
 constexpr int kQueue = DS_QUEUE;  // per-warp append staging (overflow spills to global)
 #ifndef DS_HEAVY_RED
@@ -365,6 +369,11 @@ struct KParams {
     const Edge* Ledges;
     const long long* Hptr;
     const Edge* Hedges;
+    // per row {offset mod 2^32, degree} of the light / heavy CSR: the captures
+    // read a row's extent with ONE 8-byte load (two int64 offsets were two
+    // divergent loads per frontier vertex; the L1 wavefront rate is the bound)
+    const uint2* Linfo;
+    const uint2* Hinfo;
     PullPlan Lpull, Hpull;
     D* dist;
     D* csum;             // SMALL kernel (kCsum): per scan chunk, <= every stored value >= the window
@@ -720,13 +729,23 @@ __device__ __forceinline__ void capture_emit_cta(const KParams<M>& p, Smem<typen
     }
 }
 
+// Dense-scan register layout: a warp's scan chunk is 32 x kRangePer consecutive
+// vertices; register slot j of a lane holds the vertex scan_vertex(chunk base,
+// lane, j) -- lane-interleaved 16-byte groups, so every load instruction of the
+// warp covers 512 contiguous bytes (a lane reading its own 64 contiguous bytes
+// made each instruction touch every line of the chunk: 4x the L1 tag requests).
 template <class D>
-__device__ __forceinline__ void load_run(const D* p, D (&out)[kRangePer]);
+__device__ __forceinline__ unsigned long long scan_vertex(unsigned long long cbase, int lane, int j) {
+    constexpr int V = 16 / (int)sizeof(D);
+    return cbase + (unsigned long long)((j / V) * (32 * V) + lane * V + (j % V));
+}
+template <class D>
+__device__ __forceinline__ void load_run(const D* chunk, int lane, D (&out)[kRangePer]);
 template <>
-__device__ __forceinline__ void load_run<unsigned>(const unsigned* p, unsigned (&out)[kRangePer]) {
+__device__ __forceinline__ void load_run<unsigned>(const unsigned* chunk, int lane, unsigned (&out)[kRangePer]) {
 #pragma unroll
     for (int i = 0; i < kRangePer / 4; ++i) {
-        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(p) + i);
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(chunk) + i * 32 + lane);
         out[4 * i] = q.x;
         out[4 * i + 1] = q.y;
         out[4 * i + 2] = q.z;
@@ -734,11 +753,11 @@ __device__ __forceinline__ void load_run<unsigned>(const unsigned* p, unsigned (
     }
 }
 template <>
-__device__ __forceinline__ void load_run<unsigned long long>(const unsigned long long* p,
+__device__ __forceinline__ void load_run<unsigned long long>(const unsigned long long* chunk, int lane,
                                                              unsigned long long (&out)[kRangePer]) {
 #pragma unroll
     for (int i = 0; i < kRangePer / 2; ++i) {
-        const ulonglong2 q = __ldcg(reinterpret_cast<const ulonglong2*>(p) + i);
+        const ulonglong2 q = __ldcg(reinterpret_cast<const ulonglong2*>(chunk) + i * 32 + lane);
         out[2 * i] = q.x;
         out[2 * i + 1] = q.y;
     }
@@ -754,7 +773,7 @@ template <class M, bool SUM = false, bool UNSET = false>
 __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                               typename M::D L, typename M::D H, int* S, unsigned long long* s_counter,
                               unsigned long long n_scan, const int* old_S, unsigned long long old_count,
-                              const long long* ptr) {
+                              const uint2* ptr) {
     using D = typename M::D;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem<D>& ws = sm.w[wib];
@@ -768,32 +787,49 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
     const unsigned long long n = n_scan;
     const unsigned long long per_chunk = 32ull * kRangePer;
     const unsigned long long nchunk = (n + per_chunk - 1) / per_chunk;
-    unsigned long long local_fc = 0, local_min = ~0ull;
+    unsigned long long local_fc = 0;
+    D local_min = M::INF;  // smallest stored value beyond the window (INF: none)
+    // !SUM: per scan chunk a "settled" flag (in csum's storage): every value of
+    // the chunk is below the window, hence final -- later scans skip the chunk
+    unsigned* const chunk_done = reinterpret_cast<unsigned*>(p.csum);
     auto scan_chunk = [&](unsigned long long c) {
-        const unsigned long long v0 = c * per_chunk + (unsigned long long)lane * kRangePer;
+        const unsigned long long cbase = c * per_chunk;
         D dv[kRangePer];
-        if (v0 + kRangePer <= n) {
-            load_run<D>(p.dist + v0, dv);
+        const bool full = cbase + per_chunk <= n;
+        if (full) {
+            load_run<D>(p.dist + cbase, lane, dv);
         } else {
 #pragma unroll
-            for (int j = 0; j < kRangePer; ++j) dv[j] = v0 + j < n ? __ldcg(p.dist + v0 + j) : M::INF;
+            for (int j = 0; j < kRangePer; ++j) {
+                const unsigned long long vj = scan_vertex<D>(cbase, lane, j);
+                dv[j] = vj < n ? __ldcg(p.dist + vj) : M::INF;
+            }
         }
         unsigned hits = 0;
-        unsigned long long cmin = ~0ull;
+        D cmin = M::INF;
+        bool settled = true;
 #pragma unroll
         for (int j = 0; j < kRangePer; ++j) {
             const D d = dv[j];
             if (UNSET) {
-                if (d >= L && v0 + j < n) hits |= 1u << j;
+                if (d >= L && scan_vertex<D>(cbase, lane, j) < n) hits |= 1u << j;
                 continue;
             }
-            if (d >= H && d != M::INF && (unsigned long long)d < cmin) cmin = (unsigned long long)d;
-            if (d >= L && d < H) hits |= 1u << j;
+            const bool below = d < L;
+            const bool inw = !below && d < H;
+            if (inw) hits |= 1u << j;
+            const D beyond = (below || inw) ? M::INF : d;  // INF stays INF: "none"
+            cmin = beyond < cmin ? beyond : cmin;
+            settled = settled && below;
         }
         if (cmin < local_min) local_min = cmin;
         if (SUM && !UNSET) {  // exact bound for the chunk (no relaxation runs during this step)
-            cmin = warp_min(cmin);
-            if (lane == 0) p.csum[c] = cmin == ~0ull ? M::INF : (D)cmin;
+            unsigned long long wm = warp_min((unsigned long long)cmin);
+            if (lane == 0) p.csum[c] = (D)wm;
+        }
+        if (!SUM && !UNSET && full && __all_sync(0xffffffffu, settled)) {
+            if (lane == 0) chunk_done[c] = 1u;
+            return;
         }
         if (!__any_sync(0xffffffffu, hits != 0)) return;
         local_fc += __popc(hits);
@@ -812,9 +848,9 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
                 if (rem) {
                     const int b = __ffs(rem) - 1;
                     rem &= rem - 1;
-                    vtx[j] = (int)(v0 + b);
+                    vtx[j] = (int)scan_vertex<D>(cbase, lane, b);
                     if (UNSET) {
-                        cd[j] = (D)(v0 + b);  // the entry carries the row id
+                        cd[j] = (D)vtx[j];  // the entry carries the row id
                     } else {
                         // select, not dv[b]: a dynamic index would move dv[] to local memory
                         D x = dv[0];
@@ -829,8 +865,9 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
             for (int j = 0; j < kListPer; ++j) {
                 const bool in = vtx[j] >= 0;
                 if (in) {
-                    off[j] = __ldg(ptr + vtx[j]);
-                    deg[j] = __ldg(ptr + vtx[j] + 1) - off[j];
+                    const uint2 ri = __ldg(ptr + vtx[j]);  // {row offset mod 2^32, degree}: one load
+                    off[j] = ri.x;
+                    deg[j] = ri.y;
                 }
                 news[j] = !UNSET && in && claim_bit(p.sbits, (unsigned)vtx[j]);
             }
@@ -857,7 +894,7 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
             const unsigned long long cl = g + lane * nw;
             const D s = cl < nchunk ? __ldcg(p.csum + cl) : M::INF;
             const bool act = s < H;
-            if (!act && s != M::INF && (unsigned long long)s < local_min) local_min = (unsigned long long)s;
+            if (!act && s < local_min) local_min = s;
             unsigned mask = __ballot_sync(0xffffffffu, act);
             while (mask) {
                 const int b = __ffs(mask) - 1;
@@ -865,13 +902,26 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
                 scan_chunk(g + (unsigned long long)b * nw);
             }
         }
-    } else {
+    } else if (UNSET) {
         for (unsigned long long c = gw; c < nchunk; c += nw) scan_chunk(c);
+    } else {
+        // each lane reads the settled flag of one of the warp's next 32 chunks
+        for (unsigned long long g = gw; g < nchunk; g += 32 * nw) {
+            const unsigned long long cl = g + lane * nw;
+            const unsigned f = cl < nchunk ? ldcg(chunk_done + cl) : 1u;
+            unsigned mask = __ballot_sync(0xffffffffu, f == 0u);
+            while (mask) {
+                const int b = __ffs(mask) - 1;
+                mask &= mask - 1;
+                scan_chunk(g + (unsigned long long)b * nw);
+            }
+        }
     }
     if (UNSET) return;  // the entry / edge totals are in slot->re_packed
     wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
     const unsigned long long fc = block_reduce<0>(local_fc, sm.red);
-    const unsigned long long mn = block_reduce<1>(local_min, sm.red2);
+    const unsigned long long mn =
+        block_reduce<1>(local_min == M::INF ? ~0ull : (unsigned long long)local_min, sm.red2);
     if (threadIdx.x == 0) {
         if (fc) atomicAdd(&slot->front_count, fc);
         if (mn != ~0ull) atomicMin(&slot->next_min, mn);
@@ -903,8 +953,9 @@ __device__ void capture_unsettled(const KParams<M>& p, Smem<typename M::D>& sm, 
             const D d = in ? __ldcg(p.dist + v) : (D)0;
             const bool un = in && d >= T;
             cd[j] = (D)v;
-            off[j] = un ? __ldg(p.Hptr + v) : 0;
-            deg[j] = un ? __ldg(p.Hptr + v + 1) - off[j] : 0;
+            const uint2 ri = un ? __ldg(p.Hinfo + v) : make_uint2(0u, 0u);
+            off[j] = ri.x;
+            deg[j] = ri.y;
         }
         capture_emit_cta<M, kUnsetPer>(p, sm, slot, lane, wib, cd, off, deg);
     }
@@ -917,12 +968,20 @@ __device__ void capture_unsettled(const KParams<M>& p, Smem<typename M::D>& sm, 
 template <class M, bool APPEND_S, bool VALS, bool LOCALW = false>
 __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                              const int* list, const typename M::D* vals, unsigned long long count,
-                             const long long* ptr, unsigned* clear_bits, int* S,
-                             unsigned long long* s_counter) {
+                             const uint2* ptr, unsigned* clear_bits, int* S,
+                             unsigned long long* s_counter, unsigned long long clear_words = 0) {
     using D = typename M::D;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem<D>& ws = sm.w[wib];
     unsigned qn = 0;
+    // clear_words > 0 (large lists): the dedup bitmap is zeroed as a whole by
+    // coalesced stores instead of one divergent store per list entry
+    if (!LOCALW && clear_bits && clear_words) {
+        for (unsigned long long k = (unsigned long long)blockIdx.x * kThreads + threadIdx.x; k < clear_words;
+             k += (unsigned long long)gridDim.x * kThreads)
+            clear_bits[k] = 0u;
+        clear_bits = nullptr;
+    }
     const unsigned long long per_chunk = 32ull * kCapPer;
     const unsigned long long nchunk = (count + per_chunk - 1) / per_chunk;
     // LOCALW: only this CTA's warps take part (block-local small-frontier mode)
@@ -951,8 +1010,9 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
             } else {
                 dv[j] = in[j] ? __ldcg(p.dist + vtx[j]) : (D)0;
             }
-            off[j] = in[j] ? __ldg(ptr + vtx[j]) : 0;
-            deg[j] = in[j] ? __ldg(ptr + vtx[j] + 1) - off[j] : 0;
+            const uint2 ri = in[j] ? __ldg(ptr + vtx[j]) : make_uint2(0u, 0u);
+            off[j] = ri.x;
+            deg[j] = ri.y;
             if (in[j] && clear_bits) clear_bits[(unsigned)vtx[j] >> 5] = 0u;
         }
         if (!APPEND_S && !VALS && std::is_same<M, ModeFixed>::value) {
@@ -1589,6 +1649,13 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             for (long long k = (long long)blockIdx.x * kThreads + threadIdx.x; k < (n_scan + per - 1) / per;
                  k += stride)
                 p.csum[k] = (k == src / per) ? (D)0 : M::INF;
+        } else {
+            // settled flags of the scan chunks (capture_range)
+            unsigned* const chunk_done = reinterpret_cast<unsigned*>(p.csum);
+            const long long per = 32ll * kRangePer;
+            for (long long k = (long long)blockIdx.x * kThreads + threadIdx.x; k < (n_scan + per - 1) / per;
+                 k += stride)
+                chunk_done[k] = 0u;
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             for (int k = 0; k < 3; ++k) {
@@ -1741,7 +1808,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
             if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[bpar ^ 1] = 0;
             capture_range<M, kSum>(p, sm, &c->slot[st % 3], L, H, p.S[bpar], &c->s_count[bpar],
-                             (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount, p.Lptr);
+                             (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount, p.Linfo);
             old_scount = 0;
             if (!end_step(0, (unsigned long long)n_scan)) return;
             const unsigned long long fc = ldcg(&prev()->front_count);
@@ -1828,7 +1895,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                             b->hopmax = 0;
                         }
                         __syncthreads();
-                        capture_list<M, true, false, true>(p, sm, b, p.F[lpp], nullptr, lnf, p.Lptr,
+                        capture_list<M, true, false, true>(p, sm, b, p.F[lpp], nullptr, lnf, p.Linfo,
                                                            p.fbits[lph & 1], p.S[bpar],
                                                            &c->s_count[bpar]);
                         __syncthreads();
@@ -1879,7 +1946,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 }
                 nf = ldcg(&c->slot[sl].append_count);
                 // values travel with the list; commit them in the next capture
-                capture_list<M, true, true>(p, sm, &c->slot[st % 3], p.F[pp], p.Fv[pp], nf, p.Lptr,
+                capture_list<M, true, true>(p, sm, &c->slot[st % 3], p.F[pp], p.Fv[pp], nf, p.Linfo,
                                             p.fbits[phases & 1], p.S[bpar], &c->s_count[bpar]);
                 if (nf == 0) {
                     pos = POS_HEAVY;
@@ -1916,8 +1983,9 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             if (nf == 0) {
                 pos = POS_HEAVY;
             } else {
-                capture_list<M, true, false>(p, sm, &c->slot[st % 3], p.F[pp], nullptr, nf, p.Lptr,
-                                             p.fbits[phases & 1], p.S[bpar], &c->s_count[bpar]);
+                capture_list<M, true, false>(p, sm, &c->slot[st % 3], p.F[pp], nullptr, nf, p.Linfo,
+                                             p.fbits[phases & 1], p.S[bpar], &c->s_count[bpar],
+                                             nf >= kBulkClearMin ? (unsigned long long)(n_scan + 31) / 32 : 0ull);
                 if (!end_step(2, nf)) return;
                 re = ldcg(&prev()->re_packed);
                 pp ^= 1;
@@ -1940,7 +2008,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                         a->hopmax = 0;
                     }
                     __syncthreads();
-                    capture_list<M, false, false, true>(p, sm, a, p.S[bpar], nullptr, scount, p.Hptr,
+                    capture_list<M, false, false, true>(p, sm, a, p.S[bpar], nullptr, scount, p.Hinfo,
                                                         nullptr, nullptr, nullptr);
                     __syncthreads();
                     const unsigned long long lre = ldcg(&a->re_packed);
@@ -1966,7 +2034,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 heavy_done = ldcg(&c->hh_done) != 0;
             } else {
                 capture_list<M, false, false>(p, sm, &c->slot[st % 3], p.S[bpar], nullptr, scount,
-                                              p.Hptr, nullptr, nullptr, nullptr);
+                                              p.Hinfo, nullptr, nullptr, nullptr);
                 if (!end_step(3, scount)) return;
                 re = ldcg(&prev()->re_packed);
                 if (kLex) {
