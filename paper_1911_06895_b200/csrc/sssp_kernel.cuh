@@ -247,6 +247,20 @@ constexpr bool kHeavyRed = DS_HEAVY_RED != 0;
 #define DS_CSUM_RED 1
 #endif
 constexpr bool kCsum = DS_CSUM && !(DS_PULL_LIGHT || DS_PULL_HEAVY);
+// S (the bucket's settled set, sssp.py:191) without a membership bitmap: a
+// vertex joins S exactly once per bucket -- either the bucket scan finds it in
+// the window, or ONE push brings it from at-or-beyond hi to below hi (values
+// only decrease, atomicMin serialises the pushes, so exactly one sees
+// old >= hi > new).  That push tags its next-frontier entry (bit 31) and the
+// capture of that frontier appends the vertex to S; a tagging push that loses
+// the frontier dedup claim appends to S directly.  Replaces one returning
+// atomicOr per frontier vertex and phase plus one atomicAnd per S member and
+// bucket.  The pull builds gate on the S bitmap and keep the claims.
+#ifndef DS_S_ENTRY
+#define DS_S_ENTRY 1
+#endif
+constexpr bool kSEntry = DS_S_ENTRY && !(DS_PULL_LIGHT || DS_PULL_HEAVY);
+constexpr unsigned kSTag = 0x80000000u;
 #ifndef DS_ROWMAP_SCAN
 #define DS_ROWMAP_SCAN 1  // 1: push row map by marks + warp max-scan (0: search + walk)
 #endif
@@ -780,9 +794,11 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
     unsigned qn = 0;
     const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
     const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
-    for (unsigned long long i = gw * 32 + lane; i < old_count; i += nw * 32) {
-        const unsigned v = (unsigned)ldcg(old_S + i);
-        atomicAnd(p.sbits + (v >> 5), ~(1u << (v & 31)));
+    if (!kSEntry) {
+        for (unsigned long long i = gw * 32 + lane; i < old_count; i += nw * 32) {
+            const unsigned v = (unsigned)ldcg(old_S + i);
+            atomicAnd(p.sbits + (v >> 5), ~(1u << (v & 31)));
+        }
     }
     const unsigned long long n = n_scan;
     const unsigned long long per_chunk = 32ull * kRangePer;
@@ -869,7 +885,8 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
                     off[j] = ri.x;
                     deg[j] = ri.y;
                 }
-                news[j] = !UNSET && in && claim_bit(p.sbits, (unsigned)vtx[j]);
+                // kSEntry: the scan meets every vertex once -- no claim needed
+                news[j] = !UNSET && in && (kSEntry || claim_bit(p.sbits, (unsigned)vtx[j]));
             }
             if (!UNSET) {
 #pragma unroll
@@ -965,7 +982,7 @@ __device__ void capture_unsettled(const KParams<M>& p, Smem<typename M::D>& sm, 
 // ended the previous phase (VALS: the list carries values produced by a pull
 // and this step commits them to t first), looks up degrees in `ptr`, clears
 // the next-frontier dedup bits for their next use, optionally adds to S.
-template <class M, bool APPEND_S, bool VALS, bool LOCALW = false>
+template <class M, bool APPEND_S, bool VALS, bool LOCALW = false, bool HOPS = false>
 __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                              const int* list, const typename M::D* vals, unsigned long long count,
                              const uint2* ptr, unsigned* clear_bits, int* S,
@@ -1002,6 +1019,15 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
             vtx[j] = in[j] ? ldcg(list + idx) : 0;
             if (VALS) dv[j] = in[j] ? __ldcg(vals + idx) : (D)0;
         }
+        bool tagged[kCapPer];  // kSEntry: the entry's push brought the vertex into the window
+#pragma unroll
+        for (int j = 0; j < kCapPer; ++j) {
+            tagged[j] = false;
+            if (kSEntry && APPEND_S) {
+                tagged[j] = in[j] && ((unsigned)vtx[j] & kSTag);
+                vtx[j] = (int)((unsigned)vtx[j] & ~kSTag);
+            }
+        }
         long long off[kCapPer], deg[kCapPer];
 #pragma unroll
         for (int j = 0; j < kCapPer; ++j) {
@@ -1015,7 +1041,7 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
             deg[j] = ri.y;
             if (in[j] && clear_bits) clear_bits[(unsigned)vtx[j] >> 5] = 0u;
         }
-        if (!APPEND_S && !VALS && std::is_same<M, ModeFixed>::value) {
+        if (HOPS && std::is_same<M, ModeFixed>::value) {
             // lex mode, S capture of an internal bucket: its largest hop count
             // (S holds the bucket's final keys)
             if (p.lex) {
@@ -1027,7 +1053,8 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
         if (APPEND_S) {
             bool news[kCapPer];
 #pragma unroll
-            for (int j = 0; j < kCapPer; ++j) news[j] = in[j] && claim_bit(p.sbits, (unsigned)vtx[j]);
+            for (int j = 0; j < kCapPer; ++j)
+                news[j] = kSEntry ? tagged[j] : (in[j] && claim_bit(p.sbits, (unsigned)vtx[j]));
 #pragma unroll
             for (int j = 0; j < kCapPer; ++j)
                 wq_push<D, false>(ws.q, queue_vals(ws), qn, news[j], vtx[j], (D)0, lane, S, nullptr, s_counter);
@@ -1037,7 +1064,7 @@ __device__ void capture_list(const KParams<M>& p, Smem<typename M::D>& sm, StepS
         capture_emit_cta<M, kCapPer>(p, sm, slot, lane, wib, dv, off, deg);
     }
     if (APPEND_S) wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
-    if (!APPEND_S && !VALS && std::is_same<M, ModeFixed>::value && p.lex) {
+    if (HOPS && std::is_same<M, ModeFixed>::value && p.lex) {
 #pragma unroll
         for (int o = 16; o; o >>= 1) hop_cta = max(hop_cta, __shfl_xor_sync(0xffffffffu, hop_cta, o));
         if (lane == 0 && hop_cta) atomicMax(&slot->hopmax, hop_cta);  // once per warp and capture
@@ -1073,11 +1100,17 @@ __device__ __forceinline__ void csum_lower(const KParams<M>& p, unsigned v, type
 // pulled form of the heavy relaxation, r = A_H^T (t o S) (sssp.py:206-227),
 // restricted to the rows it can still lower.  See the direction choice at
 // POS_HEAVY for why this is exact.
-template <class M, bool LIGHT, bool LOCALW = false, bool SUM = false, bool PULL = false, bool LEX = false>
+// STAG (light, kSEntry): the push that brings a vertex from at-or-beyond H to
+// below H tags its next-frontier entry with kSTag (the capture of that list
+// appends the vertex to S); if it loses the dedup claim it appends to
+// S[sidx] directly.
+template <class M, bool LIGHT, bool LOCALW = false, bool SUM = false, bool PULL = false, bool LEX = false,
+          bool STAG = false>
 __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                            unsigned long long E, unsigned long long Rc,
                            const typename M::Edge* edges, typename M::D H, int* out_list,
-                           unsigned* fbits, typename M::D HD = 0) {
+                           unsigned* fbits, typename M::D HD = 0, unsigned sidx = 0) {
+    static_assert(!STAG || (LIGHT && DS_DEFER_APPEND), "S tags ride on the deferred light appends");
     using D = typename M::D;
     using Edge = typename M::Edge;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1203,10 +1236,29 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     for (int j = 0; j < kRelPer; ++j) p_col[j] = p_ret[j] = 0u;
     auto drain = [&]() {
 #pragma unroll
+        unsigned lostbits = 0;  // STAG: entered the window but lost the frontier claim (rare)
+#pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             const bool g = ((p_req >> j) & 1u) && !(p_ret[j] & (1u << (p_col[j] & 31)));
             wq_push<D, false>(ws.q, queue_vals(ws), qn, g, (int)p_col[j], (D)0, lane, out_list, nullptr,
                               &slot->append_count);
+            if (STAG && ((p_req >> j) & 1u) && !g && (p_col[j] & kSTag)) lostbits |= 1u << j;
+        }
+        if (STAG && __any_sync(0xffffffffu, lostbits != 0u)) {
+            // those go to S directly, one reservation for the warp
+            const unsigned cnt = __popc(lostbits);
+            unsigned incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            unsigned long long b = 0;
+            if (lane == 31) b = atomicAdd(&p.ctl->s_count[sidx], (unsigned long long)incl);
+            b = __shfl_sync(0xffffffffu, b, 31) + (incl - cnt);
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j)
+                if ((lostbits >> j) & 1u) p.S[sidx][b++] = (int)(p_col[j] & ~kSTag);
         }
         p_req = 0;
         if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
@@ -1348,7 +1400,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                 const unsigned v = M::col(ed[j]);
                 const bool want = 32 * j < left && nd[j] < old[j] && nd[j] < H;
                 if (SUM && 32 * j < left && nd[j] < old[j] && nd[j] >= H) csum_lower(p, v, nd[j]);
-                p_col[j] = v;
+                p_col[j] = (STAG && want && old[j] >= H) ? (v | kSTag) : v;
                 p_ret[j] = want ? atomicOr(fbits + (v >> 5), 1u << (v & 31)) : 0u;
                 p_req |= (want ? 1u : 0u) << j;
             }
@@ -1481,6 +1533,11 @@ __device__ void pull_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot
                 const unsigned u = M::col(ed[j]);
                 if (LIGHT) {
                     du[j] = __ldcg(p.dist + u);
+                    gate[j] = du[j] >= L && du[j] < H;
+                } else if (kSEntry) {
+                    // no S bitmap: S is exactly the vertices whose (final) value
+                    // lies in the window
+                    du[j] = p.dist[u];
                     gate[j] = du[j] >= L && du[j] < H;
                 } else {
                     gate[j] = (p.sbits[u >> 5] >> (u & 31)) & 1u;
@@ -1875,8 +1932,9 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                         const unsigned long long lE = lre & kMask33;
                         lesc += lE;
                         if (lE)
-                            relax_step<M, true, true, kSum>(p, sm, a, lE, lre >> kPackShift, p.Ledges, H,
-                                                      p.F[lpp], p.fbits[lph & 1]);
+                            relax_step<M, true, true, kSum, false, false, kSEntry>(
+                                p, sm, a, lE, lre >> kPackShift, p.Ledges, H, p.F[lpp], p.fbits[lph & 1], (D)0,
+                                bpar);
                         __syncthreads();
                         if (ldcg(&a->flags) & 1u) {
                             lst = kDevOverflow;
@@ -1958,8 +2016,9 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 continue;
             } else if (E > 0) {
                 escanned += E;
-                relax_step<M, true, false, kSum, false, kLex>(p, sm, &c->slot[st % 3], E, re >> kPackShift,
-                                                             p.Ledges, H, p.F[pp], p.fbits[phases & 1], HD);
+                relax_step<M, true, false, kSum, false, kLex, kSEntry>(p, sm, &c->slot[st % 3], E,
+                                                                      re >> kPackShift, p.Ledges, H, p.F[pp],
+                                                                      p.fbits[phases & 1], HD, bpar);
                 if (!end_step(1, E)) return;
                 if (const unsigned fl = ldcg(&prev()->flags) & 3u) {
                     status = (fl & 2u) ? kDevLexFail : kDevOverflow;
@@ -2008,8 +2067,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                         a->hopmax = 0;
                     }
                     __syncthreads();
-                    capture_list<M, false, false, true>(p, sm, a, p.S[bpar], nullptr, scount, p.Hinfo,
-                                                        nullptr, nullptr, nullptr);
+                    capture_list<M, false, false, true, true>(p, sm, a, p.S[bpar], nullptr, scount, p.Hinfo,
+                                                              nullptr, nullptr, nullptr);
                     __syncthreads();
                     const unsigned long long lre = ldcg(&a->re_packed);
                     int done = 0;
@@ -2033,8 +2092,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 if (status) break;
                 heavy_done = ldcg(&c->hh_done) != 0;
             } else {
-                capture_list<M, false, false>(p, sm, &c->slot[st % 3], p.S[bpar], nullptr, scount,
-                                              p.Hinfo, nullptr, nullptr, nullptr);
+                capture_list<M, false, false, false, true>(p, sm, &c->slot[st % 3], p.S[bpar], nullptr, scount,
+                                                           p.Hinfo, nullptr, nullptr, nullptr);
                 if (!end_step(3, scount)) return;
                 re = ldcg(&prev()->re_packed);
                 if (kLex) {
@@ -2152,7 +2211,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     {
         // retire the last bucket's S bits
         const unsigned long long gt = (unsigned long long)blockIdx.x * kThreads + threadIdx.x;
-        for (unsigned long long i = gt; i < old_scount; i += (unsigned long long)gridDim.x * kThreads) {
+        for (unsigned long long i = gt; !kSEntry && i < old_scount; i += (unsigned long long)gridDim.x * kThreads) {
             const unsigned v = (unsigned)ldcg(p.S[bpar ^ 1] + i);
             atomicAnd(p.sbits + (v >> 5), ~(1u << (v & 31)));
         }
@@ -2247,7 +2306,9 @@ __global__ void __launch_bounds__(kBigThreads, DS_BIG_MINB) k_big_relax(const KP
     const int pp = (int)ldcg(&c->rs_pp);
     const unsigned long long phases = ldcg(&c->rs_phases);
     if (LIGHT)
-        relax_step<M, true>(p, sm, &c->xslot, E, Rc, p.Ledges, H, p.F[pp], p.fbits[phases & 1]);
+        relax_step<M, true, false, false, false, false, kSEntry>(p, sm, &c->xslot, E, Rc, p.Ledges, H, p.F[pp],
+                                                                 p.fbits[phases & 1], (typename M::D)0,
+                                                                 (unsigned)ldcg(&c->rs_bpar));
     else
         relax_step<M, false>(p, sm, &c->xslot, E, Rc, p.Hedges, H, nullptr, nullptr);
     (void)L;
