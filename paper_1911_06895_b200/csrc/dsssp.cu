@@ -275,6 +275,12 @@ struct ds_graph {
     void* Ledges = nullptr;
     void* Hedges = nullptr;
     size_t Lcap = 0, Hcap = 0;
+    // wide windows (lex mode): every row's light then heavy edges in one
+    // array, and its {offset, degree} per row
+    void* Aedges = nullptr;
+    uint2* Ainfo = nullptr;
+    size_t Acap = 0;
+    bool wide = false;
     // scratch
     void* dist = nullptr;  // 8n bytes (either mode)
     unsigned* fbits = nullptr;  // 2 x ceil(n/32) words: next-frontier dedup
@@ -381,7 +387,7 @@ static SolveCtx main_ctx(ds_graph* g) {
 
 static void free_all(ds_graph* g) {
     void* ptrs[] = {g->indptr, g->col,  g->w,     g->Lptr,  g->Hptr,       g->Ledges, g->Hedges,
-                    g->Linfo,  g->Hinfo,
+                    g->Linfo,  g->Hinfo,  g->Aedges, g->Ainfo,
                     g->dist,   g->fbits, g->sbits, g->F0,  g->F1,  g->Fv0, g->Fv1, g->S0, g->S1, g->req, g->Rpre,
                     g->planL.rowid, g->planL.cptr, g->planL.chunk_row, g->planL.span,
                     g->planH.rowid, g->planH.cptr, g->planH.chunk_row, g->planH.span,
@@ -606,7 +612,7 @@ template <class Edge>
 __global__ void k_split_scatter(long long nnz, long long n, const long long* indptr, const int* col,
                                 const double* w, double delta, int frac, const int* perm,
                                 const long long* Lptr, const long long* Hptr, Edge* Lout,
-                                Edge* Hout) {
+                                Edge* Hout, Edge* Aout = nullptr) {
     const int lane = threadIdx.x & 31;
     const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -630,7 +636,7 @@ __global__ void k_split_scatter(long long nnz, long long n, const long long* ind
     }
     long long carry_r = r, carry_hL = -preL, carry_hH = -preH;
     long long wl = 0, wh = 0;  // light / heavy edges of this warp before the window
-    long long cur_r = -1, baseL = 0, baseH = 0;
+    long long cur_r = -1, baseL = 0, baseH = 0, degL = 0;
     for (long long e0 = e_begin; e0 < e_end; e0 += 32) {
         const long long e = e0 + lane;
         const bool valid = e < e_end;
@@ -660,9 +666,13 @@ __global__ void k_split_scatter(long long nnz, long long n, const long long* ind
                 const long long o = perm ? perm[r] : r;
                 baseL = Lptr[o];
                 baseH = Hptr[o];
+                if (Aout) degL = Lptr[o + 1] - baseL;
             }
             if (L) put_edge(Lout, baseL + (pl - hL), c, x, frac);
             if (H) put_edge(Hout, baseH + (ph - hH), c, x, frac);
+            // merged copy (wide windows): row at baseL + baseH, light part first
+            if (Aout && L) put_edge(Aout, baseL + baseH + (pl - hL), c, x, frac);
+            if (Aout && H) put_edge(Aout, baseL + baseH + degL + (ph - hH), c, x, frac);
         }
         // the row of the window's last edge may continue into the next window
         carry_r = __shfl_sync(0xffffffffu, r, 31);
@@ -798,13 +808,15 @@ __global__ void k_symmetry_sums(const long long* indptr, const int* col, const d
 }
 
 // {offset mod 2^32, degree} per row from the light / heavy row offsets
+// (Ainfo, optional: the merged array, row r at Lptr[r] + Hptr[r])
 __global__ void k_row_info(const long long* Lptr, const long long* Hptr, long long n, uint2* Linfo,
-                           uint2* Hinfo) {
+                           uint2* Hinfo, uint2* Ainfo) {
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n;
          r += (long long)gridDim.x * blockDim.x) {
         const long long l0 = Lptr[r], l1 = Lptr[r + 1], h0 = Hptr[r], h1 = Hptr[r + 1];
         Linfo[r] = make_uint2((unsigned)l0, (unsigned)(l1 - l0));
         Hinfo[r] = make_uint2((unsigned)h0, (unsigned)(h1 - h0));
+        if (Ainfo) Ainfo[r] = make_uint2((unsigned)(l0 + h0), (unsigned)((l1 - l0) + (h1 - h0)));
     }
 }
 
@@ -1445,8 +1457,15 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     // (high-diameter) kernel and the pull builds keep the reference schedule.
     g->lex = false;
     g->ksub = 1;
-    if (mode == DS_MODE_FIXED32 && !no_lex && !g->small && !(DS_PULL_LIGHT || DS_PULL_HEAVY)) {
+    // High-diameter graphs (g->small) take lex mode with ksub = 1 and wide
+    // windows from the start when they can (thousands of tiny buckets merge
+    // into windows of up to 62: grid 2048^2 246 -> 102 ms); otherwise the
+    // block-local kernel.  DS_SMALL=1 in the environment keeps that kernel.
+    const char* sm_env = getenv("DS_SMALL");
+    const bool small_lex = g->small && !(sm_env && atoi(sm_env) != 0);
+    if (mode == DS_MODE_FIXED32 && !no_lex && (!g->small || small_lex) && !(DS_PULL_LIGHT || DS_PULL_HEAVY)) {
         int k = want_k;
+        if (g->small) k = 1;
         if (k <= 0) {
             // auto: about 3 light edges per active vertex per internal bucket
             // (light degree scales with the bucket width for uniform-ish
@@ -1457,11 +1476,17 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
             while (k < 64 && ldeg / (3.0 * k) >= 1.4142) k *= 2;  // k = 2^round(log2(ldeg / 3))
             if (g->nnz < (1ll << 28)) k = 1;  // measured: R-MAT 22 (128 M edges) +22% in lex mode, R-MAT 24 -11%
         }
+        // ksub = 1 (the reference's own buckets, keys with hop counts) only
+        // pays through the wide windows of the tail (sssp_kernel.cuh)
+        const char* wde = getenv("DS_WIDE");
+        const char* lmin = getenv("DS_LEX1_MIN_NNZ");
+        const bool k1_ok = want_k == 1 || (!(wde && atoi(wde) == 0) && g->nnz < (1LL << 32) &&
+                                           g->nnz >= (lmin ? atoll(lmin) : 0LL));
         k = (k >= 1 && k <= 64) ? 1 << (31 - __builtin_clz((unsigned)k)) : k;  // power of two
         const double X = ldexp(delta, frac);  // delta in weight units (exact: power-of-2 scale)
         // keys hold D < 2^26 - 1: every weight must be below that bound too
         const bool w_ok = ldexp(maxw, frac) < (double)ds::kLexDLimit;
-        if (k >= 2 && k <= 64 && X >= 2.0 * k && X < 1073741824.0 && w_ok) {
+        if (k >= (k1_ok ? 1 : 2) && k <= 64 && X >= 2.0 * k && X < 1073741824.0 && w_ok) {
             g->lex = true;
             g->ksub = k;
             g->WD = (unsigned)floor(X);  // w <= delta  <=>  W <= floor(delta * 2^frac)
@@ -1470,9 +1495,10 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
             // and HD - LD <= ceil(X) + 1
             const double q = ceil((ceil(X) + 1.0) / k);
             g->delta_int = ldexp(q - 1.0, -frac);  // light_int: 0 < w <= (q - 1) 2^-frac
+            if (k == 1) g->delta_int = delta;  // the reference's split (heavy W >= WD + 1 >= HD - LD)
         }
     }
-    if (g->lex) {
+    if (g->lex && g->ksub > 1) {
         // the device split: internal light / heavy (reference counts kept for
         // PrepInfo and ds_export_split)
         *g->h_pstat = init;
@@ -1491,7 +1517,7 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
         g->minH = INFINITY;
         if (si.min_heavy_bits != ~0ull) memcpy(&g->minH, &si.min_heavy_bits, 8);
     }
-    const double split_delta = g->lex ? g->delta_int : delta;
+    const double split_delta = (g->lex && g->ksub > 1) ? g->delta_int : delta;
     // phase ceiling (sssp.py:268-274), saturating
     long long per = 2;
     if (g->nL) {
@@ -1506,15 +1532,40 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
     if (g->nL >= (1LL << 32) || g->nH >= (1LL << 32))
         return set_err(DS_EINVAL, "light or heavy edge count %lld exceeds 2^32",
                        std::max(g->nL, g->nH));
-    k_row_info<<<grid, 256, 0, g->stream>>>(g->Lptr, g->Hptr, n, g->Linfo, g->Hinfo);
-    CK(cudaGetLastError());
     const size_t esz = mode == DS_MODE_FIXED32 ? sizeof(uint2) : sizeof(EdgeF64);
+    // wide windows (sssp_kernel.cuh): lex mode only; needs the merged copy of
+    // the rows (8 B per edge more) -- skipped when it does not fit
+    g->wide = false;
+    if (g->lex && g->nL + g->nH < (1LL << 32) && g->nL + g->nH > 0) {
+        const char* e = getenv("DS_WIDE");
+        if (!(e && atoi(e) == 0)) {
+            const size_t need = esz * (size_t)(g->nL + g->nH);
+            size_t fr = 0, tot = 0;
+            bool fits = need <= g->Acap;
+            // ... and only when a third of the device stays free for the caller
+            // (R-MAT 27 on one GPU keeps the narrow schedule: the copy is 34 GB)
+            // and the copy itself is at most a sixth of it (DS_WIDE=2 lifts that: R-MAT 27
+            // on one GPU is 34 GB of copy next to ~100 GB of graph)
+            if (!fits && cudaMemGetInfo(&fr, &tot) == cudaSuccess)
+                fits = need + tot / 3 < fr + g->Acap && (need <= tot / 6 || (e && atoi(e) == 2));
+            if (fits) {
+                if (!g->Ainfo) CK(cudaMalloc(&g->Ainfo, sizeof(uint2) * n));
+                if ((rc = ensure_edges(&g->Aedges, &g->Acap, need))) return rc;
+                g->wide = true;
+            }
+        }
+    }
+    if (g->small && g->lex && !g->wide) g->lex = false;  // no merged copy: the block-local kernel
+    k_row_info<<<grid, 256, 0, g->stream>>>(g->Lptr, g->Hptr, n, g->Linfo, g->Hinfo,
+                                            g->wide ? g->Ainfo : nullptr);
+    CK(cudaGetLastError());
     if ((rc = ensure_edges(&g->Ledges, &g->Lcap, esz * (size_t)g->nL))) return rc;
     if ((rc = ensure_edges(&g->Hedges, &g->Hcap, esz * (size_t)g->nH))) return rc;
     if (mode == DS_MODE_FIXED32)
         k_split_scatter<uint2><<<grid, 256, 0, g->stream>>>(g->nnz, n, g->indptr, g->col, g->w, split_delta,
                                                             g->frac, g->perm, g->Lptr, g->Hptr,
-                                                            (uint2*)g->Ledges, (uint2*)g->Hedges);
+                                                            (uint2*)g->Ledges, (uint2*)g->Hedges,
+                                                            g->wide ? (uint2*)g->Aedges : nullptr);
     else
         k_split_scatter<EdgeF64><<<grid, 256, 0, g->stream>>>(g->nnz, n, g->indptr, g->col, g->w, split_delta, 0,
                                                               g->perm, g->Lptr, g->Hptr,
@@ -1634,6 +1685,35 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     p.Hedges = (const typename M::Edge*)g->Hedges;
     p.Linfo = g->Linfo;
     p.Hinfo = g->Hinfo;
+    p.Aedges = nullptr;
+    p.Ainfo = nullptr;
+    if (g->wide && g->lex) {
+        p.Aedges = (const typename M::Edge*)g->Aedges;
+        p.Ainfo = g->Ainfo;
+        // thresholds in pushed edges per bucket / window, scaled to the share
+        // of the device this launch runs on (a step is latency-bound below a
+        // few thousand edges per warp)
+        const double share = (double)grid / (double)std::max(1u, full_grid(g));
+        auto envd = [](const char* k, double d) {
+            const char* e = getenv(k);
+            return e ? atof(e) : d;
+        };
+        p.wide_enter = (unsigned long long)std::min(1e18, envd("DS_WIDE_ENTER", 1e18) * share);
+        p.wide_lo = (unsigned long long)std::min(1e18, envd("DS_WIDE_LO", 8e6) * share);
+        p.wide_hi = (unsigned long long)std::min(1e18, envd("DS_WIDE_HI", 64e6) * share);
+        p.wide_g0 = (unsigned)std::max(1.0, envd("DS_WIDE_G0", 8));
+        p.wide_gmax = (unsigned)std::min(envd("DS_WIDE_GMAX", 1e9), (double)((ds::kWideRef - 2) * g->ksub));
+        p.wide_gmax = std::max(p.wide_gmax, 1u);
+        p.wide_force = envd("DS_WIDE_FORCE", 0) != 0;
+        if (g->small) {  // high-diameter graphs: wide from the second bucket on, largest windows
+            p.wide_force = 1;
+            p.wide_g0 = (unsigned)std::min((double)p.wide_gmax, envd("DS_WIDE_G0", 1e9));
+            p.wide_hi = (unsigned long long)std::min(1e18, envd("DS_WIDE_HI", 1e18));
+        }
+        p.wide_unsettled = (unsigned long long)(envd("DS_WIDE_FRAC", 0.25) * (double)g->nH);
+        p.wide_all = (unsigned long long)envd("DS_WIDE_ALL", 128e6);
+        p.wide_g0 = std::min(p.wide_g0, p.wide_gmax);
+    }
     p.dist = (typename M::D*)x.dist;
     p.fbits[0] = x.fbits;
     p.fbits[1] = x.fbits + g->nwords;
@@ -1763,7 +1843,7 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
     x.launches = 0;
     for (int hop = 0;; ++hop) {
         ++x.launches;
-        if (g->small)
+        if (g->small && !p.lex)
             CK(cudaLaunchKernelEx(&cfg, sssp_persistent_kernel<M, true>, p));
         else if (std::is_same<M, ModeFixed>::value && p.lex)
             CK(cudaLaunchKernelEx(&cfg, lex_kernel<M>(), p));
@@ -1831,6 +1911,8 @@ static int finish_solve(ds_graph* g, SolveCtx& x, int* dev_status) {
                         (double)(c.t_exit - last[0]) / 1e3);
         }
     }
+    if (c.wide_windows && getenv("DS_DEBUG_PREP"))
+        fprintf(stderr, "[ds] wide windows %llu, edges pushed in them %llu\n", c.wide_windows, c.wide_edges);
     if (c.cnt_atomics && getenv("DS_DEBUG_PREP"))
         fprintf(stderr, "[ds] light atomics %llu, improving %llu, edges scanned %llu\n", c.cnt_atomics,
                 c.cnt_improved, c.edges_scanned);

@@ -330,6 +330,11 @@ struct Ctl {
     unsigned long long hh_re, hh_done, hh_status;
     unsigned long long t_enter, t_exit;  // DS_TRACE: kernel entry / last CTA's finalize end
     unsigned lexsat;  // lex mode: a final key held an out-of-range sum (rerun without lex)
+    // wide windows (lex mode): per reference bucket of the window, 1 + the
+    // largest final hop count (0: no final value in the bucket); two sets,
+    // alternating between windows
+    unsigned whm[2][64];
+    unsigned long long wide_windows, wide_edges;  // stats: windows run wide / edges they pushed
 };
 
 enum : int { POS_FRESH = 0, POS_BUCKET = 1, POS_PHASE = 2, POS_AFTER_LIGHT = 3, POS_HEAVY = 4,
@@ -388,6 +393,16 @@ struct KParams {
     // divergent loads per frontier vertex; the L1 wavefront rate is the bound)
     const uint2* Linfo;
     const uint2* Hinfo;
+    // wide windows (lex mode; see "wide windows" at the solver loop): every
+    // row of A in solver order, light edges first (null: disabled)
+    const Edge* Aedges;
+    const uint2* Ainfo;
+    unsigned long long wide_enter;  // a bucket that pushed fewer edges than this switches to wide windows
+    unsigned long long wide_lo, wide_hi;  // a window below wide_lo doubles the next one, above wide_hi halves it
+    unsigned wide_g0, wide_gmax;  // first / largest window, in internal buckets
+    int wide_force;               // tests: wide windows after the first bucket, whatever its size
+    unsigned long long wide_unsettled;  // ... and at most this many heavy edges in rows not yet settled
+    unsigned long long wide_all;        // at most this many: the first window takes the largest size
     PullPlan Lpull, Hpull;
     D* dist;
     D* csum;             // SMALL kernel (kCsum): per scan chunk, <= every stored value >= the window
@@ -410,6 +425,8 @@ struct KParams {
     unsigned long long trace_cap;
     unsigned long long* cta_done;  // DS_TRACE=2: per step and CTA, the time its warps finished the step
 };
+
+constexpr int kWideRef = 64;  // reference buckets one wide window may span
 
 template <class D>
 struct WarpSmem {
@@ -453,6 +470,14 @@ struct Smem {
     unsigned long long red2[kWarps];
     int ok;
     LexAcc lx;
+    // wide windows: D thresholds of the window's reference buckets (wn + 1
+    // entries) and the per-bucket hop maxima of the hop pass
+    unsigned wthr[kWideRef + 1];
+    unsigned whm[kWideRef];
+    int wn;
+    int wfail;
+    unsigned wpar;             // which Ctl::whm set the current window reports into
+    unsigned long long bwork;  // edges pushed by the current bucket / window (thread 0 adds)
 };
 static_assert(kWarps <= 32, "one warp scans the CTA's per-warp totals");
 
@@ -1104,13 +1129,20 @@ __device__ __forceinline__ void csum_lower(const KParams<M>& p, unsigned v, type
 // below H tags its next-frontier entry with kSTag (the capture of that list
 // appends the vertex to S); if it loses the dedup claim it appends to
 // S[sidx] directly.
+// WIDE (lex mode, light): the window spans several reference buckets, so the
+// hop rule's bound -- the upper end of the SOURCE's reference bucket -- is
+// looked up per captured entry in the window's threshold table (sm.wthr) and
+// kept as an index in the warp's rel[] slots (no entry pipelining: the wide
+// steps are latency-bound tails with about one chunk per warp).
 template <class M, bool LIGHT, bool LOCALW = false, bool SUM = false, bool PULL = false, bool LEX = false,
-          bool STAG = false>
+          bool STAG = false, bool WIDE = false>
 __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
                            unsigned long long E, unsigned long long Rc,
                            const typename M::Edge* edges, typename M::D H, int* out_list,
                            unsigned* fbits, typename M::D HD = 0, unsigned sidx = 0) {
     static_assert(!STAG || (LIGHT && DS_DEFER_APPEND), "S tags ride on the deferred light appends");
+    static_assert(!WIDE || (LIGHT && LEX && !PULL && DS_ROWMAP_SCAN), "wide windows: lex-mode light pushes");
+    constexpr bool kPipe = DS_PIPE != 0 && !WIDE;
     using D = typename M::D;
     using Edge = typename M::Edge;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1164,7 +1196,19 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             // the entry of chunk_start[c + 1] may begin exactly at the next chunk
             if (rel < kChunk) ws.row[rel < 0 ? 0 : rel] = (unsigned short)k;
             ws.base[k] = en.y + (unsigned)cb;
-            ws.d[k] = __ldcg(p.Rd + r);
+            const D dk = __ldcg(p.Rd + r);
+            ws.d[k] = dk;
+            if constexpr (WIDE) {
+                // upper end of the reference bucket holding the entry's distance
+                const unsigned Du = (unsigned)(dk >> kHopBits);
+                int a = 0, b = sm.wn;
+                while (b - a > 1) {
+                    const int m = (a + b) >> 1;
+                    if (sm.wthr[m] <= Du) a = m;
+                    else b = m;
+                }
+                ws.rel[k] = (short)(a + 1);  // index of that bound in sm.wthr (rel[] is free: DS_ROWMAP_SCAN)
+            }
         }
         __syncwarp();
         {
@@ -1225,9 +1269,9 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         __syncwarp();
 #endif
     };
-#if DS_PIPE
-    if (gw < nchunk) load_meta(gw);
-#endif
+    if constexpr (kPipe) {
+        if (gw < nchunk) load_meta(gw);
+    }
     // DS_DEFER_APPEND (light): a chunk's dedup claims are consumed (appended)
     // only after the next chunk's edge loads are out, hiding their round trip
     unsigned p_col[kRelPer], p_ret[kRelPer];
@@ -1266,18 +1310,19 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     };
     for (unsigned long long c = gw; c < nchunk; c += nw) {
         const long long cb = (long long)(c * kChunk);
-#if !DS_PIPE
-        load_meta(c);
-#endif
+        if constexpr (!kPipe) load_meta(c);
         const long long left = (long long)E - cb - lane;  // edge j exists iff 32 j < left
         Edge ed[kRelPer];
+        int kk[kRelPer];  // !kPipe: the edges' entries
 #if DS_PIPE
+        if constexpr (kPipe) {
         // issue this chunk's edge loads, park the per-edge source values in
         // smem, then fetch the next chunk's entries while the edges are in flight
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             const int r = lane + 32 * j;
             const int kj = ws.row[r];
+            kk[j] = 0;
             // unconditional definition: a conditionally assigned ed[] is
             // loop-carried and was spilled to local memory
             ed[j] = (32 * j < left) ? M::load(edges + (unsigned)(ws.base[kj] + r), pol) : Edge{};
@@ -1285,9 +1330,9 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         }
         __syncwarp();
         if (c + nw < nchunk) load_meta(c + nw);
-#define DS_DU(j) ws.du[lane + 32 * (j)]
-#else
-        int kk[kRelPer];
+        } else
+#endif
+        {
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             const int r = lane + 32 * j;
@@ -1312,8 +1357,13 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                          : "memory");
         }
 #endif
+        }
+#if DS_PIPE
+#define DS_DU(j) (kPipe ? ws.du[lane + 32 * (j)] : ws.d[kk[j]])
+#else
 #define DS_DU(j) ws.d[kk[j]]
 #endif
+#define DS_HD(j) (WIDE ? (D)sm.wthr[ws.rel[kk[j]]] : HD)
         if constexpr (PULL) {
             // gather: source value t[u] (settled iff < H; settled values are
             // final, so an L1 copy is exact) and the row's own value (a stale
@@ -1351,7 +1401,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             cur[j] = (D)0;
             nd[j] = (D)0;  // defined on every path (see ed[] above)
             if (32 * j < left) {
-                if (padd<LEX>(p, DS_DU(j), ed[j], HD, nd[j])) {
+                if (padd<LEX>(p, DS_DU(j), ed[j], DS_HD(j), nd[j])) {
                     // a stale (L1) value is >= the current one: it can only
                     // cause a redundant atomic, never a missed improvement
                     const unsigned v = M::col(ed[j]);
@@ -1433,6 +1483,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         }
         __syncwarp();
 #undef DS_DU
+#undef DS_HD
     }
     if (LIGHT && DS_DEFER_APPEND) drain();
     // DS_LATE_FLUSH: appends stay in the warp queue across chunks until it
@@ -1633,6 +1684,41 @@ __device__ void commit_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSl
 
 // ---------------------------------------------------------------- the solver
 
+// Wide windows (lex mode).  The hop-count keys make the reference's counters a
+// function of the final keys alone, so the schedule is free: once the buckets
+// get small (the latency-bound tail of a power-law graph: ~75 us of barriers
+// and round trips per bucket for a few thousand improving vertices) the solver
+// merges G internal buckets into one window [L, H) and runs ONE closure over
+// it that pushes every edge of a frontier row (A, not A_L: a window wider than
+// the light threshold has no "heavy lands beyond" guarantee, and needs no
+// heavy step).  Pushes landing below H join the next frontier, the rest only
+// lower t -- label-correcting, same least fixpoint of the (D, h) keys.  After
+// the closure one pass over the window's S (every vertex whose final key lies
+// in it) takes the largest hop count per REFERENCE bucket, from which the
+// bucket's phase count and visit follow as in the narrow schedule.
+template <class M>
+__device__ void wide_hop_pass(const KParams<M>& p, Smem<typename M::D>& sm, const int* S,
+                              unsigned long long count, unsigned* out) {
+    for (int j = threadIdx.x; j < kWideRef; j += kThreads) sm.whm[j] = 0u;
+    __syncthreads();
+    const int wn = sm.wn;
+    const unsigned long long stride = (unsigned long long)gridDim.x * kThreads;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * kThreads + threadIdx.x; i < count; i += stride) {
+        const unsigned v = (unsigned)ldcg(S + i);
+        const unsigned long long key = (unsigned long long)__ldcg(p.dist + v);
+        const unsigned Du = (unsigned)(key >> kHopBits);
+        int a = 0, b = wn;
+        while (b - a > 1) {
+            const int m = (a + b) >> 1;
+            if (sm.wthr[m] <= Du) a = m;
+            else b = m;
+        }
+        atomicMax(&sm.whm[a], (unsigned)(key & kHopMask) + 1u);
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < wn && sm.whm[threadIdx.x]) atomicMax(out + threadIdx.x, sm.whm[threadIdx.x]);
+}
+
 // Window of internal bucket idx: keys [L, H) and the reference bucket's upper
 // bound HD in distance units.  Classic: idx is the reference bucket (keys =
 // distances).  Lex: reference bucket idx / ksub split into ksub integer
@@ -1738,6 +1824,10 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     unsigned bpar = 0;
     int pos = POS_BUCKET;
     bool resumed = false;
+    // wide windows (lex mode; no giant-push handoff there, so not saved)
+    // (the window's parity and edge count live in shared memory: registers are scarce here)
+    unsigned wideG = 0;  // internal buckets per window (0: the narrow schedule)
+
     if (pos0 != POS_FRESH) {
         st = ldcg(&c->rs_st);
         nbar = ldcg(&c->rs_nbar);
@@ -1819,6 +1909,8 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     constexpr bool kLex = LEX && std::is_same<M, ModeFixed>::value && !SMALL;
     static_assert(!LEX || kLex, "lex mode: fixed point, non-SMALL kernel only");
     if (kLex && threadIdx.x == 0) {
+        sm.wpar = 0u;
+        sm.bwork = 0ull;
         sm.lx.cur_ref = -1;
         sm.lx.phases = sm.lx.visited = 0;
         sm.lx.hop_acc = 0;
@@ -1839,7 +1931,39 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         D L, H, HD;
         double lo, hi;  // the reference bucket's bounds (f64)
         lex_window<M>(p, kLex, idx, lo, hi, L, H, HD);
-        if (kLex) {
+        const bool wide = kLex && wideG != 0;
+        if (kLex && wide) {
+            // window = internal buckets [idx, idx + wideG)
+            D L2, HD2;
+            double lo2, hi2;
+            lex_window<M>(p, true, idx + (long long)wideG - 1, lo2, hi2, L2, H, HD2);
+            if (pos == POS_BUCKET) {
+                // thresholds of the reference buckets it spans (kept for the
+                // window's pushes and its hop pass)
+                const long long r0 = idx >> p.ksub_log2;
+                const int wn = (int)(((idx + (long long)wideG - 1) >> p.ksub_log2) - r0 + 1);
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    sm.wn = wn;
+                    sm.wfail = 0;
+                }
+                __syncthreads();
+                if ((int)threadIdx.x < wn) {
+                    D a, b;
+                    M::window((double)(r0 + threadIdx.x) * p.delta, (double)(r0 + threadIdx.x + 1) * p.delta,
+                              p.frac, a, b);
+                    sm.wthr[threadIdx.x] = (unsigned)a;
+                    if ((int)threadIdx.x == wn - 1) sm.wthr[wn] = (unsigned)b;
+                    // same rounding corner as below, for every bucket of the window
+                    if ((unsigned long long)b - a > (unsigned long long)p.WD + 1ull) sm.wfail = 1;
+                }
+                __syncthreads();
+                if (sm.wfail) {
+                    status = kDevLexFail;
+                    break;
+                }
+            }
+        } else if (kLex) {
             D LD, HD2;
             M::window(lo, hi, p.frac, LD, HD2);
             if ((unsigned long long)HD - LD > (unsigned long long)p.WD + 1ull) {
@@ -1865,8 +1989,9 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             // ---- bucket extraction: t_Bi = {v : lo <= t[v] < hi}; S starts empty
             if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[bpar ^ 1] = 0;
             capture_range<M, kSum>(p, sm, &c->slot[st % 3], L, H, p.S[bpar], &c->s_count[bpar],
-                             (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount, p.Linfo);
+                             (unsigned long long)n_scan, p.S[bpar ^ 1], old_scount, wide ? p.Ainfo : p.Linfo);
             old_scount = 0;
+            if (kLex && threadIdx.x == 0) sm.bwork = 0ull;
             if (!end_step(0, (unsigned long long)n_scan)) return;
             const unsigned long long fc = ldcg(&prev()->front_count);
             re = ldcg(&prev()->re_packed);
@@ -1895,7 +2020,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 continue;
             }
             ++visited;
-            if (kLex && threadIdx.x == 0) sm.lx.any = 1;
+            if (kLex && !wide && threadIdx.x == 0) sm.lx.any = 1;
             pos = POS_PHASE;
         }
 
@@ -2016,9 +2141,22 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 continue;
             } else if (E > 0) {
                 escanned += E;
-                relax_step<M, true, false, kSum, false, kLex, kSEntry>(p, sm, &c->slot[st % 3], E,
-                                                                      re >> kPackShift, p.Ledges, H, p.F[pp],
-                                                                      p.fbits[phases & 1], HD, bpar);
+                if (kLex && threadIdx.x == 0) sm.bwork += E;
+                if constexpr (kLex) {
+                    if (wide)
+                        relax_step<M, true, false, false, false, true, kSEntry, true>(
+                            p, sm, &c->slot[st % 3], E, re >> kPackShift, p.Aedges, H, p.F[pp],
+                            p.fbits[phases & 1], HD, bpar);
+                    else
+                        relax_step<M, true, false, kSum, false, kLex, kSEntry>(p, sm, &c->slot[st % 3], E,
+                                                                              re >> kPackShift, p.Ledges, H,
+                                                                              p.F[pp], p.fbits[phases & 1], HD,
+                                                                              bpar);
+                } else {
+                    relax_step<M, true, false, kSum, false, kLex, kSEntry>(p, sm, &c->slot[st % 3], E,
+                                                                          re >> kPackShift, p.Ledges, H, p.F[pp],
+                                                                          p.fbits[phases & 1], HD, bpar);
+                }
                 if (!end_step(1, E)) return;
                 if (const unsigned fl = ldcg(&prev()->flags) & 3u) {
                     status = (fl & 2u) ? kDevLexFail : kDevOverflow;
@@ -2042,8 +2180,9 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             if (nf == 0) {
                 pos = POS_HEAVY;
             } else {
-                capture_list<M, true, false>(p, sm, &c->slot[st % 3], p.F[pp], nullptr, nf, p.Linfo,
-                                             p.fbits[phases & 1], p.S[bpar], &c->s_count[bpar],
+                capture_list<M, true, false>(p, sm, &c->slot[st % 3], p.F[pp], nullptr, nf,
+                                             wide ? p.Ainfo : p.Linfo, p.fbits[phases & 1], p.S[bpar],
+                                             &c->s_count[bpar],
                                              nf >= kBulkClearMin ? (unsigned long long)(n_scan + 31) / 32 : 0ull);
                 if (!end_step(2, nf)) return;
                 re = ldcg(&prev()->re_packed);
@@ -2057,6 +2196,57 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             // ---- heavy relaxation from S with current t (sssp.py:218-227)
             scount = ldcg(&c->s_count[bpar]);
             bool heavy_done = false;
+            if (kLex && wide) {
+                // ---- end of a wide window: no heavy step (the closure pushed
+                // every edge); hop maxima per reference bucket from S
+                wide_hop_pass<M>(p, sm, p.S[bpar], scount, c->whm[sm.wpar]);
+                if (!end_step(13, scount)) return;
+                if (threadIdx.x == 0) {
+                    const long long r0 = idx >> p.ksub_log2;
+                    int sat = 0;
+                    for (int j = 0; j < sm.wn; ++j) {
+                        const unsigned v = ldcg(&c->whm[sm.wpar][j]);
+                        if (!v) continue;  // no final value in this reference bucket
+                        if (v - 1u >= kHopMask) sat = 1;  // a final hop count saturated
+                        if (r0 + j != sm.lx.cur_ref) {
+                            ref_flush();
+                            sm.lx.cur_ref = r0 + j;
+                        }
+                        sm.lx.any = 1;
+                        sm.lx.hop_acc = max(sm.lx.hop_acc, v - 1u);
+                    }
+                    sm.wfail = sat;
+                    if (blockIdx.x == 0) {
+                        // the other set was last read two barriers ago
+                        for (int j = 0; j < kWideRef; ++j) c->whm[sm.wpar ^ 1u][j] = 0u;
+                        ++c->wide_windows;
+                        c->wide_edges += sm.bwork;
+                    }
+                    sm.wpar ^= 1u;
+                }
+                __syncthreads();
+                if (sm.wfail) {
+                    status = kDevLexFail;
+                    break;
+                }
+                if (sm.lx.over) {
+                    status = 2;  // DS_ENOCONVERGE: the reference's phase count
+                    break;
+                }
+                old_scount = scount;
+                bpar ^= 1;
+                idx += (long long)wideG;
+                pos = POS_BUCKET;
+                // next window: double while the windows stay latency-bound,
+                // halve (and finally return to the narrow schedule) when one
+                // pushed a throughput-sized amount of edges
+                {
+                    const unsigned long long bw = sm.bwork;  // reset only after the next window's barriers
+                    if (bw < p.wide_lo) wideG = min(wideG * 2u, p.wide_gmax);
+                    else if (bw > p.wide_hi) wideG = wideG / 2u;
+                }
+                continue;
+            }
             if (SMALL && scount <= p.local_entries) {
                 // block-local heavy step: CTA 0 captures S and, if small, relaxes it
                 if (blockIdx.x == 0) {
@@ -2107,6 +2297,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             }
             const unsigned long long E = heavy_done ? 0ull : (re & kMask33);
             hset += re & kMask33;  // S's rows are settled: their heavy edges leave the pull volume
+            if (kLex && threadIdx.x == 0) sm.bwork += E;
             // ---- direction choice.  The push streams E = |A_H rows of S|; the
             // pull streams only the rows that can still change (t >= H), whose
             // heavy edges are U = nnz(A_H) - (heavy edges of every settled row).
@@ -2186,6 +2377,15 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             bpar ^= 1;
             ++idx;
             pos = POS_BUCKET;
+            // small bucket and most of the graph settled (by heavy edges): the
+            // rest is a latency-bound tail -- wide windows from here
+            // (sm.bwork: thread 0's last add precedes the heavy step's barrier)
+            if (kLex && p.Aedges) {
+                const unsigned long long U = p.nH - min(hset, p.nH);  // heavy edges of the unsettled rows
+                if (p.wide_force) wideG = p.wide_g0;
+                else if (sm.bwork < p.wide_enter && U <= p.wide_unsettled)
+                    wideG = U <= p.wide_all ? p.wide_gmax : p.wide_g0;
+            }
         }
     }
 

@@ -98,3 +98,53 @@ def test_lex_batch_matches_single(lex_k):
             assert (stats[i].outer_iterations, stats[i].inner_phases) == (st.outer_iterations, st.inner_phases)
     finally:
         g.close()
+
+
+# ---- wide windows: the lex-mode tail merges internal buckets into one window
+# whose closure pushes every edge (sssp_kernel.cuh "wide windows"); forced from
+# the second bucket on here, with growing and shrinking window sizes.
+@pytest.fixture(params=["grow", "shrink", "fixed3"])
+def wide_mode(request, monkeypatch):
+    monkeypatch.setenv("DS_LEX_K", "2")
+    monkeypatch.setenv("DS_WIDE_FORCE", "1")
+    if request.param == "grow":
+        monkeypatch.setenv("DS_WIDE_G0", "1")
+        monkeypatch.setenv("DS_WIDE_LO", "1e18")  # every window doubles the next one
+    elif request.param == "shrink":
+        monkeypatch.setenv("DS_WIDE_G0", "7")
+        monkeypatch.setenv("DS_WIDE_LO", "0")
+        monkeypatch.setenv("DS_WIDE_HI", "100")  # halves down to the narrow schedule and re-enters
+    else:
+        monkeypatch.setenv("DS_WIDE_G0", "3")
+        monkeypatch.setenv("DS_WIDE_LO", "0")
+        monkeypatch.setenv("DS_WIDE_HI", "1e18")
+    clear_device_cache()
+    yield request.param
+    clear_device_cache()
+
+
+def test_wide_windows_rmat(wide_mode):
+    a = graphs.rmat(15, seed=3, weight_seed=4)
+    for d in (0.05, 0.1, 0.25):
+        for s in graphs.pick_sources(a.indptr, 3, seed=23):
+            _check(a, int(s), d)
+
+
+def test_wide_windows_er_and_grid(wide_mode):
+    a = graphs.erdos_renyi(1024, seed=0)  # directed, integer weights
+    for d in (3.0, 10.0):
+        for s in (0, 17):
+            _check(a, s, d)
+    g = graphs.grid2d(48, seed=2)  # many reference buckets per window
+    _check(g, 0, 25.0)
+
+
+def test_wide_windows_golden_corpus(wide_mode, golden):
+    for (a, s, kind), rec in list(zip(criterion1_graphs(), golden["criterion1"]))[::11]:
+        for run in rec["runs"]:
+            d = float.fromhex(run["delta"])
+            r = delta_stepping(a, s, d)
+            assert vec_hash(r.distances.indices, r.distances.values) == run["hash"]
+            assert (r.outer_iterations, r.inner_phases) == (run["outer"], run["phases"])
+            rs = delta_stepping(a, s, d, skip_empty_buckets=True)
+            assert (rs.outer_iterations, rs.inner_phases) == (run["outer_skip"], run["phases_skip"])

@@ -64,8 +64,17 @@ def _certify(g, d_h, s):
 def test_rmat27_fixpoint_certificate():
     # a fresh process: the graph (~100 GB) plus the certificate's device copy
     # of the CSR (~50 GB) need the device to themselves
+    import gc
     import subprocess
 
+    import torch
+
+    from paper_1911_06895_b200 import clear_device_cache
+
+    # nothing of the earlier tests may stay resident in this (parent) process
+    clear_device_cache()
+    gc.collect()
+    torch.cuda.empty_cache()
     r = subprocess.run([sys.executable, __file__], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "certified" in r.stdout

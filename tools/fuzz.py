@@ -40,13 +40,29 @@ base_env = dict(os.environ)
 
 
 def knobs():
-    """Random solver knobs: lex mode forced with ksub 1..8, the heavy gather
-    forced on small graphs (any ratio) or off."""
+    """Random solver knobs: lex mode forced with ksub 1..8 (and there wide
+    windows off / forced with random growth), the heavy gather forced on small
+    graphs (any ratio) or off."""
     env = dict(base_env)
     lk = int(rng.integers(0, 5))
     if lk:
         env["DS_LEX"] = "1"
         env["DS_LEX_K"] = str(1 << (lk - 1))
+    wd = int(rng.integers(0, 4)) if lk else 0
+    for k in ("DS_WIDE", "DS_WIDE_FORCE", "DS_WIDE_G0", "DS_WIDE_LO", "DS_WIDE_HI"):
+        env.pop(k, None)
+    if wd == 1:
+        env["DS_WIDE"] = "0"
+    elif wd >= 2:
+        # wide windows from the second bucket on: growing (LO huge), shrinking
+        # back to the narrow schedule (HI tiny), or at the default thresholds
+        env["DS_WIDE_FORCE"] = "1"
+        env["DS_WIDE_G0"] = str(int(rng.choice([1, 2, 3, 7])))
+        gr = int(rng.integers(0, 3))
+        if gr == 0:
+            env["DS_WIDE_LO"] = "1e18"
+        elif gr == 1:
+            env["DS_WIDE_LO"] = "0"; env["DS_WIDE_HI"] = str(int(rng.choice([0, 50, 2000])))
     hp = int(rng.integers(0, 3))
     if hp == 1:
         env["DS_HPULL_MIN"] = "0"
@@ -55,7 +71,8 @@ def knobs():
         env["DS_HPULL"] = "0"
     os.environ.clear()
     os.environ.update(env)
-    return f"lex={env.get('DS_LEX_K', '-')} hpull={hp}"
+    return (f"lex={env.get('DS_LEX_K', '-')} hpull={hp} wide={wd} g0={env.get('DS_WIDE_G0', '-')} "
+            f"lo={env.get('DS_WIDE_LO', '-')} hi={env.get('DS_WIDE_HI', '-')}")
 
 
 while time.time() < t_end:

@@ -8,7 +8,8 @@ side = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 a = graphs.grid2d(side, seed=3)
 g = DeviceGraph.from_matrix(a)
 names = ["scan", "light_relax", "light_capture", "heavy_capture", "heavy_relax", "light_pull",
-         "light_commit", "heavy_pull", "heavy_commit", "light_local", "heavy_local"]
+         "light_commit", "heavy_pull", "heavy_commit", "light_local", "heavy_local", "unsettled_capture",
+         "heavy_gather", "hop_pass"]
 g.solve(0, 25.0)
 st = g.solve(0, 25.0)
 cap = 1 << 20
