@@ -1467,14 +1467,22 @@ static int prepare(ds_graph* g, double delta, uint32_t flags) {
         int k = want_k;
         if (g->small) k = 1;
         if (k <= 0) {
-            // auto: about 3 light edges per active vertex per internal bucket
+            // auto: about 1.5 light edges per active vertex per internal bucket
             // (light degree scales with the bucket width for uniform-ish
-            // weights), rounded to a power of two; small graphs are
-            // latency-bound (more buckets cost more than re-pushes save)
+            // weights), rounded to a power of two.  With the tail merged into
+            // wide windows the extra buckets only exist where they save
+            // re-pushes (R-MAT 24, 4 in flight: delta 0.1 k 2/4/8 = 174/194/180
+            // GTEPS, delta 0.25 k 4/8 = 156/190, delta 0.05 k 1/2/4 = 173/195/179;
+            // 3 per bucket was the optimum of the narrow-only schedule).
             const double ldeg = g->n_active > 0 ? (double)g->refL / (double)g->n_active : 0.0;
+            const char* per = getenv("DS_LEX_PER");
+            const double target = per ? atof(per) : 1.5;
             k = 1;
-            while (k < 64 && ldeg / (3.0 * k) >= 1.4142) k *= 2;  // k = 2^round(log2(ldeg / 3))
-            if (g->nnz < (1ll << 28)) k = 1;  // measured: R-MAT 22 (128 M edges) +22% in lex mode, R-MAT 24 -11%
+            while (k < 64 && ldeg / (target * k) >= 1.4142) k *= 2;  // k = 2^round(log2(ldeg / target))
+            // small graphs are latency-bound (more buckets cost more than re-pushes save)
+            const char* kmin = getenv("DS_LEXK_MIN_NNZ");
+            // (R-MAT 18: k auto 0.66 vs 0.61 ms at k 1; R-MAT 20 batch 94 vs 77 GTEPS, R-MAT 22 122 vs 87)
+            if (g->nnz < (kmin ? atoll(kmin) : (1ll << 24))) k = 1;
         }
         // ksub = 1 (the reference's own buckets, keys with hop counts) only
         // pays through the wide windows of the tail (sssp_kernel.cuh)
