@@ -1718,7 +1718,7 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
             p.wide_g0 = (unsigned)std::min((double)p.wide_gmax, envd("DS_WIDE_G0", 1e9));
             p.wide_hi = (unsigned long long)std::min(1e18, envd("DS_WIDE_HI", 1e18));
         }
-        p.wide_unsettled = (unsigned long long)(envd("DS_WIDE_FRAC", 0.25) * (double)g->nH);
+        p.wide_unsettled = (unsigned long long)(envd("DS_WIDE_FRAC", 0.125) * (double)g->nH);
         p.wide_all = (unsigned long long)envd("DS_WIDE_ALL", 128e6);
         p.wide_g0 = std::min(p.wide_g0, p.wide_gmax);
     }

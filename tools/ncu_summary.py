@@ -4,6 +4,7 @@ traffic_bytes_per_launch from the newest one)."""
 import csv, json, sys
 
 raw, out, command = sys.argv[1], sys.argv[2], sys.argv[3]
+workload = sys.argv[4] if len(sys.argv) > 4 else "rmat24_ef16_delta0.1, bench pool source 0 (tools/one_source.py)"
 rows = list(csv.reader(open(raw)))
 hdr, data = rows[0], rows[2:]
 col = {h: i for i, h in enumerate(hdr)}
@@ -45,7 +46,7 @@ for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             L[key] *= scale
 tot = sum((L["dram_read"] or 0) + (L["dram_write"] or 0) for L in launches)
 json.dump({
-    "workload": "rmat24_ef16_delta0.1, bench pool source 0 (tools/one_source.py)",
+    "workload": workload,
     "command": command,
     "launches_of_one_source": launches,
     "gpu_time_ms": sum(L["ms"] for L in launches),
