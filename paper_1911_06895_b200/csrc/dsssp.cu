@@ -1713,6 +1713,7 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         p.wide_gmax = (unsigned)std::min(envd("DS_WIDE_GMAX", 1e9), (double)((ds::kWideRef - 2) * g->ksub));
         p.wide_gmax = std::max(p.wide_gmax, 1u);
         p.wide_force = envd("DS_WIDE_FORCE", 0) != 0;
+        p.bidir = envd("DS_BIDIR", 1) != 0 && g->symmetric;
         if (g->small) {  // high-diameter graphs: wide from the second bucket on, largest windows
             p.wide_force = 1;
             p.wide_g0 = (unsigned)std::min((double)p.wide_gmax, envd("DS_WIDE_G0", 1e9));

@@ -401,6 +401,7 @@ struct KParams {
     unsigned long long wide_lo, wide_hi;  // a window below wide_lo doubles the next one, above wide_hi halves it
     unsigned wide_g0, wide_gmax;  // first / largest window, in internal buckets
     int wide_force;               // tests: wide windows after the first bucket, whatever its size
+    int bidir;                    // enter the wide tail through the bidirectional step
     unsigned long long wide_unsettled;  // ... and at most this many heavy edges in rows not yet settled
     unsigned long long wide_all;        // at most this many: the first window takes the largest size
     PullPlan Lpull, Hpull;
@@ -976,11 +977,19 @@ __device__ void capture_range(const KParams<M>& p, Smem<typename M::D>& sm, Step
 // reservation per CTA round.  Entries carry the row id; rows >= n_scan and
 // rows without heavy edges get none.
 constexpr int kUnsetPer = 4;
+// `info`: the rows' extents (A_H, or the merged rows for the bidirectional
+// step).  S != null: rows whose value already lies in [T, HW) -- reached by
+// light pushes beyond the bucket -- are appended to S (the coming wide
+// window's settled set; everything else enters it by a tagged push).
 template <class M>
 __device__ void capture_unsettled(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
-                                  typename M::D T, unsigned long long n_scan) {
+                                  typename M::D T, unsigned long long n_scan, const uint2* info,
+                                  typename M::D HW = 0, int* S = nullptr,
+                                  unsigned long long* s_counter = nullptr) {
     using D = typename M::D;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem<D>& ws = sm.w[wib];
+    unsigned qn = 0;
     const unsigned long long per_warp = 32ull * kUnsetPer;
     const unsigned long long nblk = (n_scan + per_warp - 1) / per_warp;
     const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
@@ -995,12 +1004,14 @@ __device__ void capture_unsettled(const KParams<M>& p, Smem<typename M::D>& sm, 
             const D d = in ? __ldcg(p.dist + v) : (D)0;
             const bool un = in && d >= T;
             cd[j] = (D)v;
-            const uint2 ri = un ? __ldg(p.Hinfo + v) : make_uint2(0u, 0u);
+            const uint2 ri = un ? __ldg(info + v) : make_uint2(0u, 0u);
             off[j] = ri.x;
             deg[j] = ri.y;
+            if (S) wq_push<D, false>(ws.q, queue_vals(ws), qn, un && d < HW, (int)v, (D)0, lane, S, nullptr, s_counter);
         }
         capture_emit_cta<M, kUnsetPer>(p, sm, slot, lane, wib, cd, off, deg);
     }
+    if (S) wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, S, nullptr, s_counter);
 }
 
 // LIST capture: a frontier / S list.  Snapshots d after the barrier that
@@ -1117,6 +1128,44 @@ __device__ __forceinline__ void csum_lower(const KParams<M>& p, unsigned v, type
 #endif
 }
 
+// Row map of a warp chunk from the entries' start marks: every chunk edge takes
+// the largest mark at or before it (one warp max-scan instead of a per-lane
+// search and walk).  ws.row holds the marks on entry, the entry index per edge
+// on return; the caller syncs the warp around it.
+template <class D>
+__device__ __forceinline__ void rowmap_scan(WarpSmem<D>& ws, int lane) {
+    static_assert(kRelPer == 8 || kRelPer == 4, "row-map scan: 4 or 8 edges per lane");
+    unsigned w[kRelPer / 2];  // the lane's kRelPer marks, two per word
+    if constexpr (kRelPer == 8) {
+        const uint4 m4 = reinterpret_cast<uint4*>(ws.row)[lane];
+        w[0] = m4.x; w[1] = m4.y; w[2] = m4.z; w[3] = m4.w;
+    } else {
+        const uint2 m2 = reinterpret_cast<uint2*>(ws.row)[lane];
+        w[0] = m2.x; w[1] = m2.y;
+    }
+    unsigned v[kRelPer];
+#pragma unroll
+    for (int j = 0; j < kRelPer; ++j) v[j] = (j & 1) ? (w[j / 2] >> 16) : (w[j / 2] & 0xFFFFu);
+#pragma unroll
+    for (int j = 1; j < kRelPer; ++j) v[j] = max(v[j], v[j - 1]);
+    unsigned run = v[kRelPer - 1];  // inclusive max-scan of the lanes' maxima
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, run, o);
+        if (lane >= o) run = max(run, t);
+    }
+    unsigned carry = __shfl_up_sync(0xffffffffu, run, 1);
+    if (lane == 0) carry = 0;
+#pragma unroll
+    for (int j = 0; j < kRelPer; ++j) v[j] = max(v[j], carry);
+#pragma unroll
+    for (int j = 0; j < kRelPer / 2; ++j) w[j] = v[2 * j] | (v[2 * j + 1] << 16);
+    if constexpr (kRelPer == 8)
+        reinterpret_cast<uint4*>(ws.row)[lane] = make_uint4(w[0], w[1], w[2], w[3]);
+    else
+        reinterpret_cast<uint2*>(ws.row)[lane] = make_uint2(w[0], w[1]);
+}
+
 // SUM: also lower the scan-chunk bound of every target that may have received
 // a value beyond the window (SMALL kernel, see capture_range).
 // PULL (heavy only): the entries are the UNSETTLED rows v (capture_range
@@ -1211,37 +1260,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
             }
         }
         __syncwarp();
-        {
-            unsigned w[kRelPer / 2];  // the lane's kRelPer marks, two per word
-            if constexpr (kRelPer == 8) {
-                const uint4 m4 = reinterpret_cast<uint4*>(ws.row)[lane];
-                w[0] = m4.x; w[1] = m4.y; w[2] = m4.z; w[3] = m4.w;
-            } else {
-                const uint2 m2 = reinterpret_cast<uint2*>(ws.row)[lane];
-                w[0] = m2.x; w[1] = m2.y;
-            }
-            unsigned v[kRelPer];
-#pragma unroll
-            for (int j = 0; j < kRelPer; ++j) v[j] = (j & 1) ? (w[j / 2] >> 16) : (w[j / 2] & 0xFFFFu);
-#pragma unroll
-            for (int j = 1; j < kRelPer; ++j) v[j] = max(v[j], v[j - 1]);
-            unsigned run = v[kRelPer - 1];  // inclusive max-scan of the lanes' maxima
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned t = __shfl_up_sync(0xffffffffu, run, o);
-                if (lane >= o) run = max(run, t);
-            }
-            unsigned carry = __shfl_up_sync(0xffffffffu, run, 1);
-            if (lane == 0) carry = 0;
-#pragma unroll
-            for (int j = 0; j < kRelPer; ++j) v[j] = max(v[j], carry);
-#pragma unroll
-            for (int j = 0; j < kRelPer / 2; ++j) w[j] = v[2 * j] | (v[2 * j + 1] << 16);
-            if constexpr (kRelPer == 8)
-                reinterpret_cast<uint4*>(ws.row)[lane] = make_uint4(w[0], w[1], w[2], w[3]);
-            else
-                reinterpret_cast<uint2*>(ws.row)[lane] = make_uint2(w[0], w[1]);
-        }
+        rowmap_scan<D>(ws, lane);
         __syncwarp();
 #else
         for (int k = lane; k < ne; k += 32) {
@@ -1490,6 +1509,189 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     // is half full, so most chunks skip the reservation round trip
     if (LIGHT) wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
     if (__any_sync(0xffffffffu, overflow) && lane == 0) atomicOr(&slot->flags, LEX ? 2u : 1u);
+}
+
+// ---------------------------------------------------------------- bidirectional step
+//
+// Entry into the wide tail (lex mode, symmetric graphs), replacing the heavy
+// gather + the window's scan + its first push round.  Entries are the
+// UNSETTLED rows v (value >= HN) over the merged rows (A); one pass reads
+// t[u] for every edge (v,u) ONCE and uses it in both directions:
+//  A  gather: u settled (t[u] < HN) contributes t[u] + w to v (the bucket's
+//     heavy step; the light edges of settled sources were pushed with their
+//     final values already, so re-applying them is a no-op);
+//  B  per entry: the row's value after A (rows lying inside this warp chunk
+//     are complete; rows crossing a chunk boundary join the next frontier
+//     when they hold a value in the window, and push from there);
+//  C  push back: t[v] + w to every neighbour it improves -- the window's
+//     first round, with t[u] from A as the pre-check.
+// Every edge between two unsettled rows is seen from both ends, and a vertex
+// lowered after its own row was processed joins the next frontier, so after
+// the step "t[b] <= t[a] + w, or a is in the frontier" holds for every edge:
+// the wide window continues with ordinary rounds.  S of the window: rows
+// already inside it at the capture (capture_unsettled), plus the one atomic
+// that brings a vertex from at-or-beyond HW to below it (returned old value).
+template <class M>
+__device__ void bidir_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlot* slot,
+                           unsigned long long E, unsigned long long Rc, typename M::D HN,
+                           typename M::D HW, typename M::D HD, int* out_list, unsigned* fbits,
+                           unsigned sidx) {
+    using D = typename M::D;
+    using Edge = typename M::Edge;
+    static_assert(kRelPer == 8 && DS_ROWMAP_SCAN, "bidirectional step: 256-edge chunks, scanned row map");
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    WarpSmem<D>& ws = sm.w[wib];
+    unsigned qn = 0;
+    const unsigned long long nchunk = (E + kChunk - 1) / kChunk;
+    const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + wib;
+    const unsigned long long nw = (unsigned long long)gridDim.x * kWarps;
+    const unsigned long long pol = evict_first_policy();
+    // one reservation per warp for direct S appends
+    auto s_append = [&](unsigned bits, const unsigned (&ids)[kRelPer]) {
+        if (!__any_sync(0xffffffffu, bits != 0u)) return;
+        const unsigned cnt = __popc(bits);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        unsigned long long b = 0;
+        if (lane == 31) b = atomicAdd(&p.ctl->s_count[sidx], (unsigned long long)incl);
+        b = __shfl_sync(0xffffffffu, b, 31) + (incl - cnt);
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j)
+            if ((bits >> j) & 1u) p.S[sidx][b++] = (int)ids[j];
+    };
+    for (unsigned long long c = gw; c < nchunk; c += nw) {
+        const long long cb = (long long)(c * kChunk);
+        const unsigned long long r0 = ldcg(p.chunk_start + c);
+        const unsigned long long r1 = (c + 1 < nchunk) ? ldcg(p.chunk_start + c + 1) : Rc - 1;
+        const int ne = (int)(r1 - r0 + 1);
+        reinterpret_cast<uint4*>(ws.row)[lane] = make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+        for (int k = lane; k < ne; k += 32) {
+            const unsigned long long r = r0 + k;
+            const uint2 en = __ldcg(p.Rent + r);
+            const long long rel = (long long)en.x - cb;
+            if (rel < kChunk) ws.row[rel < 0 ? 0 : rel] = (unsigned short)k;
+            ws.base[k] = en.y + (unsigned)cb;
+            ws.d[k] = __ldcg(p.Rd + r);  // the row id
+            // the row ends where the next entry starts (the step's last row at E)
+            const long long end = (r + 1 < Rc) ? (long long)__ldcg(p.Rent + r + 1).x : (long long)E;
+            ws.rel[k] = (short)((rel >= 0 && end - cb <= kChunk) ? 1 : 0);  // 1: the whole row lies in this chunk
+        }
+        __syncwarp();
+        rowmap_scan<D>(ws, lane);
+        __syncwarp();
+        const long long left = (long long)E - cb - lane;  // edge j exists iff 32 j < left
+        Edge ed[kRelPer];
+        int kk[kRelPer];
+        unsigned row[kRelPer];
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j) {
+            const int r = lane + 32 * j;
+            kk[j] = ws.row[r];
+            ed[j] = (32 * j < left) ? M::load(p.Aedges + (unsigned)(ws.base[kk[j]] + r), pol) : Edge{};
+            row[j] = (unsigned)ws.d[kk[j]];
+        }
+        D du[kRelPer];
+        // ---- A: gather from the settled neighbours
+        {
+            D cur[kRelPer];
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                du[j] = M::INF;
+                cur[j] = (D)0;
+                if (32 * j < left) {
+                    du[j] = p.dist[M::col(ed[j])];  // settled values are final; others only pre-check (stale is >=)
+                    cur[j] = p.dist[row[j]];
+                }
+            }
+            unsigned sbits = 0;
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                if (32 * j < left && du[j] < HN) {
+                    D nd;
+                    padd<true>(p, du[j], ed[j], HD, nd);
+                    if (nd < cur[j]) {
+                        const D old = atomicMin(p.dist + row[j], nd);  // returning: complete before B reads
+                        if (old >= HW && nd < HW) sbits |= 1u << j;     // the one atomic that brings it in
+                    }
+                }
+            }
+            s_append(sbits, row);
+        }
+        __syncwarp();
+        // ---- B: the rows' values after A
+        for (int k0 = 0; k0 < ne; k0 += 32) {
+            const int k = k0 + lane;
+            bool fr = false;
+            unsigned v = 0;
+            if (k < ne) {
+                v = (unsigned)ws.d[k];
+                const bool whole = ws.rel[k] != 0;
+                const D tv = __ldcg(p.dist + v);
+                D keep = M::INF;
+                if (tv < HW) {
+                    if (whole) {
+                        keep = tv;
+                        const unsigned Du = (unsigned)(tv >> kHopBits);
+                        int a = 0, b = sm.wn;
+                        while (b - a > 1) {
+                            const int m = (a + b) >> 1;
+                            if (sm.wthr[m] <= Du) a = m;
+                            else b = m;
+                        }
+                        ws.rel[k] = (short)(a + 1);  // the bound of its reference bucket, in sm.wthr
+                    } else {
+                        fr = claim_bit(fbits, v);  // crosses a chunk boundary: pushes from the next frontier
+                    }
+                }
+                ws.d[k] = keep;
+            }
+            wq_push<D, false>(ws.q, queue_vals(ws), qn, fr, (int)v, (D)0, lane, out_list, nullptr,
+                              &slot->append_count);
+        }
+        __syncwarp();
+        // ---- C: push back
+        {
+            D nd[kRelPer], old[kRelPer];
+            unsigned tgt[kRelPer];
+            unsigned want = 0;
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                nd[j] = old[j] = (D)0;
+                tgt[j] = M::col(ed[j]);
+                const D tv = ws.d[kk[j]];
+                if (32 * j < left && tv != M::INF) {
+                    padd<true>(p, tv, ed[j], (D)sm.wthr[ws.rel[kk[j]]], nd[j]);
+                    old[j] = nd[j];
+                    if (nd[j] < du[j]) old[j] = atomicMin(p.dist + tgt[j], nd[j]);
+                    if (nd[j] < old[j] && nd[j] < HW) want |= 1u << j;
+                }
+            }
+            unsigned ret[kRelPer];
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j)
+                ret[j] = ((want >> j) & 1u) ? atomicOr(fbits + (tgt[j] >> 5), 1u << (tgt[j] & 31)) : 0u;
+            unsigned lost = 0;  // entered the window but lost the frontier claim: S directly
+#pragma unroll
+            for (int j = 0; j < kRelPer; ++j) {
+                const bool w = (want >> j) & 1u;
+                const bool g = w && !(ret[j] & (1u << (tgt[j] & 31)));
+                const bool tag = w && old[j] >= HW;
+                wq_push<D, false>(ws.q, queue_vals(ws), qn, g, (int)(tag ? (tgt[j] | kSTag) : tgt[j]), (D)0, lane,
+                                  out_list, nullptr, &slot->append_count);
+                if (tag && !g) lost |= 1u << j;
+            }
+            s_append(lost, tgt);
+        }
+        if (qn > (unsigned)kQueue / 2)
+            wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
+        __syncwarp();
+    }
+    wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
 }
 
 // ---------------------------------------------------------------- pull step
@@ -1927,6 +2129,30 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         sm.lx.hop_acc = 0;
     };
 
+    // thresholds of the reference buckets the window [idx0, idx0 + G) spans
+    // (kept in shared memory for the window's pushes and its hop pass); false:
+    // the rounding corner of the narrow schedule's check, in one of them
+    auto wide_setup = [&](long long idx0, unsigned G) -> bool {
+        const long long r0 = idx0 >> p.ksub_log2;
+        const int wn = (int)(((idx0 + (long long)G - 1) >> p.ksub_log2) - r0 + 1);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            sm.wn = wn;
+            sm.wfail = 0;
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < wn) {
+            D a, b;
+            M::window((double)(r0 + threadIdx.x) * p.delta, (double)(r0 + threadIdx.x + 1) * p.delta, p.frac, a,
+                      b);
+            sm.wthr[threadIdx.x] = (unsigned)a;
+            if ((int)threadIdx.x == wn - 1) sm.wthr[wn] = (unsigned)b;
+            if ((unsigned long long)b - a > (unsigned long long)p.WD + 1ull) sm.wfail = 1;
+        }
+        __syncthreads();
+        return sm.wfail == 0;
+    };
+
     for (;;) {
         D L, H, HD;
         double lo, hi;  // the reference bucket's bounds (f64)
@@ -1937,31 +2163,9 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             D L2, HD2;
             double lo2, hi2;
             lex_window<M>(p, true, idx + (long long)wideG - 1, lo2, hi2, L2, H, HD2);
-            if (pos == POS_BUCKET) {
-                // thresholds of the reference buckets it spans (kept for the
-                // window's pushes and its hop pass)
-                const long long r0 = idx >> p.ksub_log2;
-                const int wn = (int)(((idx + (long long)wideG - 1) >> p.ksub_log2) - r0 + 1);
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    sm.wn = wn;
-                    sm.wfail = 0;
-                }
-                __syncthreads();
-                if ((int)threadIdx.x < wn) {
-                    D a, b;
-                    M::window((double)(r0 + threadIdx.x) * p.delta, (double)(r0 + threadIdx.x + 1) * p.delta,
-                              p.frac, a, b);
-                    sm.wthr[threadIdx.x] = (unsigned)a;
-                    if ((int)threadIdx.x == wn - 1) sm.wthr[wn] = (unsigned)b;
-                    // same rounding corner as below, for every bucket of the window
-                    if ((unsigned long long)b - a > (unsigned long long)p.WD + 1ull) sm.wfail = 1;
-                }
-                __syncthreads();
-                if (sm.wfail) {
-                    status = kDevLexFail;
-                    break;
-                }
+            if (pos == POS_BUCKET && !wide_setup(idx, wideG)) {
+                status = kDevLexFail;
+                break;
             }
         } else if (kLex) {
             D LD, HD2;
@@ -2316,9 +2520,52 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                     Lw = L >> kHopBits;
                     Hw = H == M::INF ? (D)kLexDLimit : (D)(H >> kHopBits);
                 }
-                if ((double)E > (double)p.hpull_ratio * (double)U &&
-                    M::heavy_beyond(Lw, Hw, lo, hi, p.min_heavy)) {
-                    capture_unsettled<M>(p, sm, &c->slot[st % 3], H, (unsigned long long)n_scan);
+                bool gather = (double)E > (double)p.hpull_ratio * (double)U &&
+                              M::heavy_beyond(Lw, Hw, lo, hi, p.min_heavy);
+                if constexpr (kLex && kSEntry) {
+                    // the tail starts here: enter the wide window through the
+                    // bidirectional step (heavy gather + scan + first round in one pass)
+                    if (gather && p.Aedges && p.bidir && !p.wide_force && U <= p.wide_unsettled) {
+                        __syncthreads();  // thread 0's sm.bwork
+                        if (sm.bwork < p.wide_enter) {
+                            const unsigned G = U <= p.wide_all ? p.wide_gmax : p.wide_g0;
+                            if (!wide_setup(idx + 1, G)) {
+                                status = kDevLexFail;
+                                break;
+                            }
+                            D L2, HW, HD2;
+                            double lo2, hi2;
+                            lex_window<M>(p, true, idx + (long long)G, lo2, hi2, L2, HW, HD2);
+                            capture_unsettled<M>(p, sm, &c->slot[st % 3], H, (unsigned long long)n_scan, p.Ainfo, HW,
+                                                 p.S[bpar ^ 1], &c->s_count[bpar ^ 1]);
+                            if (!end_step(11, (unsigned long long)n_scan)) return;
+                            const unsigned long long pre = ldcg(&prev()->re_packed);
+                            const unsigned long long Ep = pre & kMask33;
+                            ++npull;
+                            ++phases;  // the window's first round (dedup bitmap parity)
+                            nf = 0;
+                            if (Ep > 0) {
+                                escanned += Ep;
+                                bidir_step<M>(p, sm, &c->slot[st % 3], Ep, pre >> kPackShift, H, HW, HD, p.F[pp],
+                                              p.fbits[phases & 1], bpar ^ 1);
+                                if (!end_step(14, Ep)) return;
+                                nf = ldcg(&prev()->append_count);
+                            }
+                            if (threadIdx.x == 0) sm.bwork = Ep;
+                            // no scan opened this window: the S counter the NEXT window will
+                            // use (this bucket's, read by every CTA barriers ago) is reset here
+                            if (blockIdx.x == 0 && threadIdx.x == 0) c->s_count[bpar] = 0;
+                            old_scount = scount;
+                            bpar ^= 1;
+                            idx += 1;
+                            wideG = G;
+                            pos = POS_AFTER_LIGHT;
+                            continue;
+                        }
+                    }
+                }
+                if (gather) {
+                    capture_unsettled<M>(p, sm, &c->slot[st % 3], H, (unsigned long long)n_scan, p.Hinfo);
                     if (!end_step(11, (unsigned long long)n_scan)) return;
                     const unsigned long long pre = ldcg(&prev()->re_packed);
                     const unsigned long long Ep = pre & kMask33;

@@ -148,3 +148,31 @@ def test_wide_windows_golden_corpus(wide_mode, golden):
             assert (r.outer_iterations, r.inner_phases) == (run["outer"], run["phases"])
             rs = delta_stepping(a, s, d, skip_empty_buckets=True)
             assert (rs.outer_iterations, rs.inner_phases) == (run["outer_skip"], run["phases_skip"])
+
+
+# ---- the bidirectional entry into the wide tail (heavy gather + the window's
+# scan + its first round in one pass), forced at the first bucket with a heavy
+# step on symmetric graphs, with whole-tail and small first windows
+@pytest.fixture(params=["all", "g3", "g1"])
+def bidir_mode(request, monkeypatch):
+    monkeypatch.setenv("DS_LEX_K", "2")
+    monkeypatch.setenv("DS_HPULL_MIN", "0")
+    monkeypatch.setenv("DS_HPULL_RATIO", "0")
+    monkeypatch.setenv("DS_WIDE_FRAC", "1.0")
+    if request.param != "all":
+        monkeypatch.setenv("DS_WIDE_ALL", "0")
+        monkeypatch.setenv("DS_WIDE_G0", request.param[1:])
+    clear_device_cache()
+    yield request.param
+    clear_device_cache()
+
+
+def test_bidirectional_entry(bidir_mode):
+    a = graphs.rmat(15, seed=3, weight_seed=4)
+    for d in (0.05, 0.1, 0.25):
+        for s in graphs.pick_sources(a.indptr, 3, seed=29):
+            _check(a, int(s), d)
+    _check(graphs.grid2d(48, seed=2), 0, 25.0)
+    b = graphs.rmat(12, seed=9, weight_seed=1)
+    for s in graphs.pick_sources(b.indptr, 4, seed=5):
+        _check(b, int(s), 0.3)

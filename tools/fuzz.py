@@ -63,6 +63,13 @@ def knobs():
             env["DS_WIDE_LO"] = "1e18"
         elif gr == 1:
             env["DS_WIDE_LO"] = "0"; env["DS_WIDE_HI"] = str(int(rng.choice([0, 50, 2000])))
+    for k in ("DS_WIDE_FRAC", "DS_WIDE_ALL", "DS_BIDIR"):
+        env.pop(k, None)
+    if lk and wd == 0 and rng.integers(0, 2):
+        # bidirectional entry reachable at the first heavy step (symmetric graphs, gather chosen)
+        env["DS_WIDE_FRAC"] = "1.0"
+        if rng.integers(0, 2):
+            env["DS_WIDE_ALL"] = "0"; env["DS_WIDE_G0"] = str(int(rng.choice([1, 2, 5])))
     hp = int(rng.integers(0, 3))
     if hp == 1:
         env["DS_HPULL_MIN"] = "0"
@@ -72,7 +79,8 @@ def knobs():
     os.environ.clear()
     os.environ.update(env)
     return (f"lex={env.get('DS_LEX_K', '-')} hpull={hp} wide={wd} g0={env.get('DS_WIDE_G0', '-')} "
-            f"lo={env.get('DS_WIDE_LO', '-')} hi={env.get('DS_WIDE_HI', '-')}")
+            f"lo={env.get('DS_WIDE_LO', '-')} hi={env.get('DS_WIDE_HI', '-')} frac={env.get('DS_WIDE_FRAC', '-')} "
+            f"all={env.get('DS_WIDE_ALL', '-')}")
 
 
 while time.time() < t_end:

@@ -10,7 +10,7 @@ delta = float(sys.argv[2]) if len(sys.argv) > 2 else 0.1
 g = DeviceGraph.rmat(scale, 16, 1, 2)
 indptr, _, _ = g.download()
 srcs = graphs.pick_sources(indptr, 3, seed=7)
-names = ["scan", "light_relax", "light_capture", "heavy_capture", "heavy_relax", "light_pull", "light_commit", "heavy_pull", "heavy_commit", "light_local", "heavy_local", "unsettled_capture", "heavy_gather", "hop_pass"]
+names = ["scan", "light_relax", "light_capture", "heavy_capture", "heavy_relax", "light_pull", "light_commit", "heavy_pull", "heavy_commit", "light_local", "heavy_local", "unsettled_capture", "heavy_gather", "hop_pass", "bidir"]
 for s in srcs:
     st = g.solve(s, delta)
     cap = 1 << 16

@@ -9,7 +9,7 @@ a = graphs.grid2d(side, seed=3)
 g = DeviceGraph.from_matrix(a)
 names = ["scan", "light_relax", "light_capture", "heavy_capture", "heavy_relax", "light_pull",
          "light_commit", "heavy_pull", "heavy_commit", "light_local", "heavy_local", "unsettled_capture",
-         "heavy_gather", "hop_pass"]
+         "heavy_gather", "hop_pass", "bidir"]
 g.solve(0, 25.0)
 st = g.solve(0, 25.0)
 cap = 1 << 20

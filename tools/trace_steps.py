@@ -6,7 +6,7 @@ from paper_1911_06895_b200 import DeviceGraph, graphs, _lib
 g = DeviceGraph.rmat(24, 16, 1, 2)
 indptr, _, _ = g.download()
 s = graphs.pick_sources(indptr, 3, seed=7)[0]
-names = ["scan", "light_relax", "light_capture", "heavy_capture", "heavy_relax", "light_pull", "light_commit", "heavy_pull", "heavy_commit", "light_local", "heavy_local", "unsettled_capture", "heavy_gather", "hop_pass"]
+names = ["scan", "light_relax", "light_capture", "heavy_capture", "heavy_relax", "light_pull", "light_commit", "heavy_pull", "heavy_commit", "light_local", "heavy_local", "unsettled_capture", "heavy_gather", "hop_pass", "bidir"]
 st = g.solve(s, 0.1)
 st = g.solve(s, 0.1)
 cap = 1 << 16
