@@ -1519,10 +1519,11 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
 // t[u] for every edge (v,u) ONCE and uses it in both directions:
 //  A  gather: u settled (t[u] < HN) contributes t[u] + w to v (the bucket's
 //     heavy step; the light edges of settled sources were pushed with their
-//     final values already, so re-applying them is a no-op);
-//  B  per entry: the row's value after A (rows lying inside this warp chunk
-//     are complete; rows crossing a chunk boundary join the next frontier
-//     when they hold a value in the window, and push from there);
+//     final values already, so re-applying them is a no-op), min-reduced per
+//     row in the warp's shared memory;
+//  B  per entry: one atomicMin commits a lowered row; rows lying inside this
+//     warp chunk are complete, rows crossing a chunk boundary join the next
+//     frontier when they hold a value in the window, and push from there;
 //  C  push back: t[v] + w to every neighbour it improves -- the window's
 //     first round, with t[u] from A as the pre-check.
 // Every edge between two unsettled rows is seen from both ends, and a vertex
@@ -1539,6 +1540,7 @@ __device__ void bidir_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
     using D = typename M::D;
     using Edge = typename M::Edge;
     static_assert(kRelPer == 8 && DS_ROWMAP_SCAN, "bidirectional step: 256-edge chunks, scanned row map");
+    static_assert(std::is_same<D, unsigned>::value, "bidirectional step: lex mode (32-bit keys)");
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     WarpSmem<D>& ws = sm.w[wib];
     unsigned qn = 0;
@@ -1587,51 +1589,48 @@ __device__ void bidir_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
         const long long left = (long long)E - cb - lane;  // edge j exists iff 32 j < left
         Edge ed[kRelPer];
         int kk[kRelPer];
-        unsigned row[kRelPer];
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             const int r = lane + 32 * j;
             kk[j] = ws.row[r];
             ed[j] = (32 * j < left) ? M::load(p.Aedges + (unsigned)(ws.base[kk[j]] + r), pol) : Edge{};
-            row[j] = (unsigned)ws.d[kk[j]];
+        }
+        __syncwarp();  // every lane holds its entries and addresses: base[] and row[] are free
+        // the rows' current values, min-reduced in shared memory by the gather
+        // (base[k]); row[k]: the gather lowered it
+        for (int k = lane; k < ne; k += 32) {
+            ws.base[k] = (unsigned)__ldcg(p.dist + (unsigned)ws.d[k]);
+            if (k < kChunk) ws.row[k] = 0;
         }
         D du[kRelPer];
+#pragma unroll
+        for (int j = 0; j < kRelPer; ++j)  // settled values are final; the rest only pre-check (stale is >=)
+            du[j] = (32 * j < left) ? p.dist[M::col(ed[j])] : M::INF;
+        __syncwarp();
         // ---- A: gather from the settled neighbours
-        {
-            D cur[kRelPer];
 #pragma unroll
-            for (int j = 0; j < kRelPer; ++j) {
-                du[j] = M::INF;
-                cur[j] = (D)0;
-                if (32 * j < left) {
-                    du[j] = p.dist[M::col(ed[j])];  // settled values are final; others only pre-check (stale is >=)
-                    cur[j] = p.dist[row[j]];
-                }
+        for (int j = 0; j < kRelPer; ++j) {
+            if (32 * j < left && du[j] < HN) {
+                D nd;
+                padd<true>(p, du[j], ed[j], HD, nd);
+                if ((unsigned)nd < atomicMin(&ws.base[kk[j]], (unsigned)nd)) ws.row[kk[j]] = 1;
             }
-            unsigned sbits = 0;
-#pragma unroll
-            for (int j = 0; j < kRelPer; ++j) {
-                if (32 * j < left && du[j] < HN) {
-                    D nd;
-                    padd<true>(p, du[j], ed[j], HD, nd);
-                    if (nd < cur[j]) {
-                        const D old = atomicMin(p.dist + row[j], nd);  // returning: complete before B reads
-                        if (old >= HW && nd < HW) sbits |= 1u << j;     // the one atomic that brings it in
-                    }
-                }
-            }
-            s_append(sbits, row);
         }
         __syncwarp();
-        // ---- B: the rows' values after A
+        // ---- B: per row, commit the gathered value; what the row does next
         for (int k0 = 0; k0 < ne; k0 += 32) {
             const int k = k0 + lane;
-            bool fr = false;
+            bool fr = false, sev = false;
             unsigned v = 0;
             if (k < ne) {
                 v = (unsigned)ws.d[k];
                 const bool whole = ws.rel[k] != 0;
-                const D tv = __ldcg(p.dist + v);
+                D tv = (D)ws.base[k];
+                if (k < kChunk && ws.row[k]) {
+                    const D old = atomicMin(p.dist + v, tv);
+                    sev = old >= HW && tv < HW;  // the one atomic that brings it into the window
+                    tv = old < tv ? old : tv;
+                }
                 D keep = M::INF;
                 if (tv < HW) {
                     if (whole) {
@@ -1648,7 +1647,14 @@ __device__ void bidir_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
                         fr = claim_bit(fbits, v);  // crosses a chunk boundary: pushes from the next frontier
                     }
                 }
-                ws.d[k] = keep;
+                ws.base[k] = (unsigned)keep;
+            }
+            const unsigned sm_ = __ballot_sync(0xffffffffu, sev);
+            if (sm_) {
+                unsigned long long b = 0;
+                if (lane == 0) b = atomicAdd(&p.ctl->s_count[sidx], (unsigned long long)__popc(sm_));
+                b = __shfl_sync(0xffffffffu, b, 0);
+                if (sev) p.S[sidx][b + __popc(sm_ & ((1u << lane) - 1u))] = (int)v;
             }
             wq_push<D, false>(ws.q, queue_vals(ws), qn, fr, (int)v, (D)0, lane, out_list, nullptr,
                               &slot->append_count);
@@ -1663,7 +1669,7 @@ __device__ void bidir_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
             for (int j = 0; j < kRelPer; ++j) {
                 nd[j] = old[j] = (D)0;
                 tgt[j] = M::col(ed[j]);
-                const D tv = ws.d[kk[j]];
+                const D tv = (D)ws.base[kk[j]];
                 if (32 * j < left && tv != M::INF) {
                     padd<true>(p, tv, ed[j], (D)sm.wthr[ws.rel[kk[j]]], nd[j]);
                     old[j] = nd[j];
