@@ -292,6 +292,11 @@ constexpr unsigned kSTag = 0x80000000u;
 #define DS_L2PF 0  // bulk L2 prefetch of the next chunk's edges (measured slower: 5.34 -> 5.40 ms)
 #endif
 
+#ifndef DS_WIDE_REF
+#define DS_WIDE_REF 256
+#endif
+constexpr int kWideRef = DS_WIDE_REF;  // reference buckets one wide window may span
+
 struct StepSlot {
     unsigned long long re_packed;     // capture: reserved (entries << 33) | edges
     unsigned long long front_count;   // capture (range mode): frontier size
@@ -333,7 +338,7 @@ struct Ctl {
     // wide windows (lex mode): per reference bucket of the window, 1 + the
     // largest final hop count (0: no final value in the bucket); two sets,
     // alternating between windows
-    unsigned whm[2][64];
+    unsigned whm[2][kWideRef];
     unsigned long long wide_windows, wide_edges;  // stats: windows run wide / edges they pushed
 };
 
@@ -426,8 +431,6 @@ struct KParams {
     unsigned long long trace_cap;
     unsigned long long* cta_done;  // DS_TRACE=2: per step and CTA, the time its warps finished the step
 };
-
-constexpr int kWideRef = 64;  // reference buckets one wide window may span
 
 template <class D>
 struct WarpSmem {
@@ -2411,11 +2414,14 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 // every edge); hop maxima per reference bucket from S
                 wide_hop_pass<M>(p, sm, p.S[bpar], scount, c->whm[sm.wpar]);
                 if (!end_step(13, scount)) return;
+                // the window's hop maxima: loaded by the CTA, accounted by thread 0
+                for (int j = threadIdx.x; j < sm.wn; j += kThreads) sm.whm[j] = ldcg(&c->whm[sm.wpar][j]);
+                __syncthreads();
                 if (threadIdx.x == 0) {
                     const long long r0 = idx >> p.ksub_log2;
                     int sat = 0;
                     for (int j = 0; j < sm.wn; ++j) {
-                        const unsigned v = ldcg(&c->whm[sm.wpar][j]);
+                        const unsigned v = sm.whm[j];
                         if (!v) continue;  // no final value in this reference bucket
                         if (v - 1u >= kHopMask) sat = 1;  // a final hop count saturated
                         if (r0 + j != sm.lx.cur_ref) {
