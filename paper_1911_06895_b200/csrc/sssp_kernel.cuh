@@ -292,6 +292,9 @@ constexpr unsigned kSTag = 0x80000000u;
 #define DS_L2PF 0  // bulk L2 prefetch of the next chunk's edges (measured slower: 5.34 -> 5.40 ms)
 #endif
 
+#ifndef DS_BIDIR_BUILD
+#define DS_BIDIR_BUILD 1  // 0: compile the bidirectional step out (register-pressure A/B)
+#endif
 #ifndef DS_WIDE_REF
 #define DS_WIDE_REF 256
 #endif
@@ -2534,7 +2537,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
                 }
                 bool gather = (double)E > (double)p.hpull_ratio * (double)U &&
                               M::heavy_beyond(Lw, Hw, lo, hi, p.min_heavy);
-                if constexpr (kLex && kSEntry) {
+                if constexpr (kLex && kSEntry && DS_BIDIR_BUILD) {
                     // the tail starts here: enter the wide window through the
                     // bidirectional step (heavy gather + scan + first round in one pass)
                     if (gather && p.Aedges && p.bidir && !p.wide_force && U <= p.wide_unsettled) {
