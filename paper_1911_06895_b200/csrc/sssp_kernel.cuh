@@ -1300,19 +1300,20 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     // DS_DEFER_APPEND (light): a chunk's dedup claims are consumed (appended)
     // only after the next chunk's edge loads are out, hiding their round trip
     unsigned p_col[kRelPer], p_ret[kRelPer];
-    unsigned p_req = 0;
+    unsigned p_req = 0, p_tag = 0;  // claims requested / of those, the pushes that brought a vertex into the window
 #pragma unroll
     for (int j = 0; j < kRelPer; ++j) p_col[j] = p_ret[j] = 0u;
     auto drain = [&]() {
-#pragma unroll
-        unsigned lostbits = 0;  // STAG: entered the window but lost the frontier claim (rare)
+        unsigned gm = 0;
 #pragma unroll
         for (int j = 0; j < kRelPer; ++j) {
             const bool g = ((p_req >> j) & 1u) && !(p_ret[j] & (1u << (p_col[j] & 31)));
             wq_push<D, false>(ws.q, queue_vals(ws), qn, g, (int)p_col[j], (D)0, lane, out_list, nullptr,
                               &slot->append_count);
-            if (STAG && ((p_req >> j) & 1u) && !g && (p_col[j] & kSTag)) lostbits |= 1u << j;
+            gm |= (g ? 1u : 0u) << j;
         }
+        // STAG: entered the window but lost the frontier claim (rare)
+        const unsigned lostbits = STAG ? (p_tag & ~gm) : 0u;
         if (STAG && __any_sync(0xffffffffu, lostbits != 0u)) {
             // those go to S directly, one reservation for the warp
             const unsigned cnt = __popc(lostbits);
@@ -1330,6 +1331,7 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                 if ((lostbits >> j) & 1u) p.S[sidx][b++] = (int)(p_col[j] & ~kSTag);
         }
         p_req = 0;
+        p_tag = 0;
         if (!DS_LATE_FLUSH || qn > (unsigned)kQueue / 2)
             wq_flush<D, false>(ws.q, queue_vals(ws), qn, lane, out_list, nullptr, &slot->append_count);
     };
@@ -1475,9 +1477,11 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
                 const unsigned v = M::col(ed[j]);
                 const bool want = 32 * j < left && nd[j] < old[j] && nd[j] < H;
                 if (SUM && 32 * j < left && nd[j] < old[j] && nd[j] >= H) csum_lower(p, v, nd[j]);
-                p_col[j] = (STAG && want && old[j] >= H) ? (v | kSTag) : v;
+                const bool tag = STAG && want && old[j] >= H;
+                p_col[j] = tag ? (v | kSTag) : v;
                 p_ret[j] = want ? atomicOr(fbits + (v >> 5), 1u << (v & 31)) : 0u;
                 p_req |= (want ? 1u : 0u) << j;
+                p_tag |= (tag ? 1u : 0u) << j;
             }
 #else
             unsigned got[kRelPer];
