@@ -2686,42 +2686,56 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
         unsigned long long cnt = 0, m = 0, mx = 0;
         const long long tid = (long long)blockIdx.x * kThreads + threadIdx.x;
         const long long stride8 = 8ll * gridDim.x * kThreads;
-        for (long long v0 = 8 * tid; v0 < p.n; v0 += stride8) {
-            int sv[8];
-            const bool full = v0 + 8 <= p.n;
-            if (full) {
-                const int4 a = __ldg(reinterpret_cast<const int4*>(p.perm + v0));
-                const int4 b = __ldg(reinterpret_cast<const int4*>(p.perm + v0) + 1);
-                sv[0] = a.x; sv[1] = a.y; sv[2] = a.z; sv[3] = a.w;
-                sv[4] = b.x; sv[5] = b.y; sv[6] = b.z; sv[7] = b.w;
-            } else {
+        // a warp converts 256 consecutive vertices per round, lane-interleaved
+        // pairs: every perm load of the warp covers 256 contiguous bytes and
+        // every output store 512 (full write combining, also when p.out is
+        // mapped host memory: zero-copy batch results)
+        {
+            const int lane = threadIdx.x & 31;
+            const long long wg = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
+            // a batch row of a caller's array is 16-byte aligned only for even n
+            const bool out_al = (reinterpret_cast<unsigned long long>(p.out) & 15ull) == 0;
+            for (long long base = wg * 256; base < p.n; base += (long long)gridDim.x * kWarps * 256) {
+                int sv[8];
+                const bool full = base + 256 <= p.n;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) sv[j] = v0 + j < p.n ? __ldg(p.perm + v0 + j) : (int)n_scan;
-            }
-            D d[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                d[j] = sv[j] < n_scan ? __ldcg(p.dist + sv[j]) : M::INF;
-                if (kLex && d[j] == (D)kLexSat) atomicOr(&c->lexsat, 1u);
-                if (kLex && d[j] != M::INF) d[j] >>= kHopBits;  // key -> distance
-            }
-            double o[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (d[j] != M::INF) {
-                    ++cnt;
-                    if ((unsigned long long)d[j] > mx) mx = (unsigned long long)d[j];
+                for (int i = 0; i < 4; ++i) {
+                    const long long v = base + i * 64 + lane * 2;
+                    if (full) {
+                        const int2 a = __ldg(reinterpret_cast<const int2*>(p.perm + v));
+                        sv[2 * i] = a.x;
+                        sv[2 * i + 1] = a.y;
+                    } else {
+                        sv[2 * i] = v < p.n ? __ldg(p.perm + v) : (int)n_scan;
+                        sv[2 * i + 1] = v + 1 < p.n ? __ldg(p.perm + v + 1) : (int)n_scan;
+                    }
                 }
-                o[j] = M::to_f64(d[j], p.frac);
-            }
-            if (full) {
-                double2* q = reinterpret_cast<double2*>(p.out + v0);
+                D d[8];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) q[j] = make_double2(o[2 * j], o[2 * j + 1]);
-            } else {
+                for (int j = 0; j < 8; ++j) {
+                    d[j] = sv[j] < n_scan ? __ldcg(p.dist + sv[j]) : M::INF;
+                    if (kLex && d[j] == (D)kLexSat) atomicOr(&c->lexsat, 1u);
+                    if (kLex && d[j] != M::INF) d[j] >>= kHopBits;  // key -> distance
+                }
+                double o[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (v0 + j < p.n) p.out[v0 + j] = o[j];
+                for (int j = 0; j < 8; ++j) {
+                    if (d[j] != M::INF) {
+                        ++cnt;
+                        if ((unsigned long long)d[j] > mx) mx = (unsigned long long)d[j];
+                    }
+                    o[j] = M::to_f64(d[j], p.frac);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const long long v = base + i * 64 + lane * 2;
+                    if (full && out_al) {
+                        *reinterpret_cast<double2*>(p.out + v) = make_double2(o[2 * i], o[2 * i + 1]);
+                    } else {
+                        if (v < p.n) p.out[v] = o[2 * i];
+                        if (v + 1 < p.n) p.out[v + 1] = o[2 * i + 1];
+                    }
+                }
             }
         }
         // m_r = sum of out-degrees of the reached vertices, in solver order
