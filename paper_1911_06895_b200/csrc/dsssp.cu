@@ -1772,6 +1772,9 @@ static int launch_solve(ds_graph* g, SolveCtx& x, long long source, unsigned gri
         const char* hm = getenv("DS_HPULL_MIN");
         p.hpull_min = hm ? (unsigned long long)atoll(hm) : (1ull << 20);
         p.nH = (unsigned long long)g->nH;
+        p.nL = (unsigned long long)g->nL;
+        p.nA = (unsigned long long)(g->nL + g->nH);
+        p.cap_chunks = (unsigned long long)(g->nnz / kChunk + 4);
         p.lex = g->lex ? 1 : 0;
         p.ksub_log2 = __builtin_ctz((unsigned)g->ksub);
         p.WD = g->WD;

@@ -50,6 +50,30 @@
 
 #include "common.cuh"
 
+// DS_CHECKS=1 builds (tools/build_variant.py chk -DDS_CHECKS=1): device-side
+// bounds checks on the indices the solver computes -- entry ranks, chunk-map
+// slots, edge offsets, targets, list lengths, window tables -- that print the
+// failing condition and trap.  compute-sanitizer is not available on the GPU
+// pool; the GPU test suite and the fuzzer run against this build instead.
+#ifndef DS_CHECKS
+#define DS_CHECKS 0
+#endif
+#if DS_CHECKS
+#include <cstdio>
+#define DS_ASSERT(cond)                                                                              \
+    do {                                                                                             \
+        if (!(cond)) {                                                                               \
+            printf("DS_ASSERT failed: %s (line %d) block %d thread %d\n", #cond, __LINE__, blockIdx.x, \
+                   threadIdx.x);                                                                     \
+            __trap();                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define DS_ASSERT(cond) \
+    do {                \
+    } while (0)
+#endif
+
 namespace ds {
 
 namespace cg = cooperative_groups;
@@ -384,6 +408,8 @@ struct KParams {
     float hpull_ratio;
     unsigned long long hpull_min;
     unsigned long long nH;
+    unsigned long long nL, nA;     // edges in A_L / the merged rows (DS_CHECKS bounds)
+    unsigned long long cap_chunks;  // slots of chunk_start (DS_CHECKS bounds)
     unsigned long long min_heavy;  // smallest heavy weight: fixed W, or f64 bits
     // Sub-bucketed solve with lexicographic keys (fixed point only; see
     // "lex mode" below): ksub internal buckets per reference bucket, dist
@@ -717,10 +743,12 @@ __device__ __forceinline__ void capture_emit(const KParams<M>& p, StepSlot* slot
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         if (deg[j] > 0) {
+            DS_ASSERT(rank < (unsigned long long)p.n);
             p.Rent[rank] = make_uint2((unsigned)pre, (unsigned)(off[j] - (long long)pre));
             p.Rd[rank] = dv[j];
             const unsigned long long t0 = (pre + kChunk - 1) / kChunk;
             const unsigned long long t1 = (pre + (unsigned long long)deg[j] - 1) / kChunk;
+            DS_ASSERT(t1 < p.cap_chunks);
             for (unsigned long long t = t0; t <= t1; ++t) p.chunk_start[t] = (unsigned)rank;
             ++rank;
             pre += (unsigned long long)deg[j];
@@ -764,10 +792,12 @@ __device__ __forceinline__ void capture_emit_cta(const KParams<M>& p, Smem<typen
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
         if (deg[j] > 0) {
+            DS_ASSERT(rank < (unsigned long long)p.n);
             p.Rent[rank] = make_uint2((unsigned)pre, (unsigned)(off[j] - (long long)pre));
             p.Rd[rank] = dv[j];
             const unsigned long long t0 = (pre + kChunk - 1) / kChunk;
             const unsigned long long t1 = (pre + (unsigned long long)deg[j] - 1) / kChunk;
+            DS_ASSERT(t1 < p.cap_chunks);
             for (unsigned long long t = t0; t <= t1; ++t) p.chunk_start[t] = (unsigned)rank;
             ++rank;
             pre += (unsigned long long)deg[j];
@@ -1214,6 +1244,9 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
     // and the row map: lane resolves the entry of chunk edges [8 lane, 8 lane + 8)
     // DS_CS_PREFETCH: the chunk map words of a warp's next chunk are loaded one
     // iteration early (two registers), taking a round trip off the chain
+#if DS_CHECKS
+    int ne_chk = 0;  // entries of the chunk in flight
+#endif
     unsigned cs0 = 0, cs1 = 0;
     auto cs_fetch = [&](unsigned long long c) {
         if (c < nchunk) {
@@ -1234,6 +1267,10 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         }
         const int ne = (int)(r1 - r0 + 1);
         const long long cb = (long long)(c * kChunk);
+        DS_ASSERT(ne >= 1 && ne <= kChunk + 1 && r1 < Rc);
+#if DS_CHECKS
+        ne_chk = ne;
+#endif
 #if DS_ROWMAP_SCAN
         // row map by marks + prefix max: entry k marks the chunk edge where
         // its row starts, then every edge takes the largest mark at or
@@ -1364,9 +1401,21 @@ __device__ DS_RELAX_INLINE void relax_step(const KParams<M>& p, Smem<typename M:
         for (int j = 0; j < kRelPer; ++j) {
             const int r = lane + 32 * j;
             kk[j] = ws.row[r];
+#if DS_CHECKS
+            if (32 * j < left) {
+                const unsigned long long lim =
+                    edges == p.Ledges ? p.nL : (edges == p.Hedges ? p.nH : (edges == p.Aedges ? p.nA : ~0ull));
+                DS_ASSERT(kk[j] < ne_chk);
+                // (the partitioned solver's parameter blocks carry no counts: 0 = unchecked)
+                DS_ASSERT(lim == 0 || (unsigned long long)(unsigned)(ws.base[kk[j]] + r) < lim);
+            }
+#endif
             // unconditional definition: a conditionally assigned ed[] is
             // loop-carried and was spilled to local memory
             ed[j] = (32 * j < left) ? M::load(edges + (unsigned)(ws.base[kk[j]] + r), pol) : Edge{};
+#if DS_CHECKS
+            if (32 * j < left) DS_ASSERT((long long)M::col(ed[j]) < p.n);
+#endif
         }
 #if DS_L2PF
         // L2 prefetch of this warp's next chunk: cs0 already holds its first
@@ -1580,6 +1629,7 @@ __device__ void bidir_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
         const unsigned long long r0 = ldcg(p.chunk_start + c);
         const unsigned long long r1 = (c + 1 < nchunk) ? ldcg(p.chunk_start + c + 1) : Rc - 1;
         const int ne = (int)(r1 - r0 + 1);
+        DS_ASSERT(ne >= 1 && ne <= kChunk + 1 && r1 < Rc);
         reinterpret_cast<uint4*>(ws.row)[lane] = make_uint4(0u, 0u, 0u, 0u);
         __syncwarp();
         for (int k = lane; k < ne; k += 32) {
@@ -1603,7 +1653,12 @@ __device__ void bidir_step(const KParams<M>& p, Smem<typename M::D>& sm, StepSlo
         for (int j = 0; j < kRelPer; ++j) {
             const int r = lane + 32 * j;
             kk[j] = ws.row[r];
+            if (32 * j < left) {
+                DS_ASSERT(kk[j] < ne && kk[j] < kChunk);
+                DS_ASSERT((unsigned long long)(unsigned)(ws.base[kk[j]] + r) < p.nA);
+            }
             ed[j] = (32 * j < left) ? M::load(p.Aedges + (unsigned)(ws.base[kk[j]] + r), pol) : Edge{};
+            if (32 * j < left) DS_ASSERT((long long)M::col(ed[j]) < p.n);
         }
         __syncwarp();  // every lane holds its entries and addresses: base[] and row[] are free
         // the rows' current values, min-reduced in shared memory by the gather
@@ -1931,6 +1986,8 @@ __device__ void wide_hop_pass(const KParams<M>& p, Smem<typename M::D>& sm, cons
             if (sm.wthr[m] <= Du) a = m;
             else b = m;
         }
+        DS_ASSERT(a >= 0 && a < wn && wn <= kWideRef && (long long)v < p.n);
+        DS_ASSERT(Du >= sm.wthr[0] && Du < sm.wthr[wn]);  // every S member's final key lies in the window
         atomicMax(&sm.whm[a], (unsigned)(key & kHopMask) + 1u);
     }
     __syncthreads();
@@ -2078,6 +2135,15 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
             s->next_min = ~0ull;
         }
         const bool ok = grid_sync(c, gen, deadline, sm);
+#if DS_CHECKS
+        if (ok && blockIdx.x == 0 && threadIdx.x == 0) {  // the step's list lengths fit their arrays
+            const StepSlot* s = &c->slot[st % 3];
+            DS_ASSERT(ldcg(&s->append_count) <= (unsigned long long)p.n);
+            DS_ASSERT((ldcg(&s->re_packed) >> kPackShift) <= (unsigned long long)p.n);
+            DS_ASSERT((ldcg(&s->re_packed) & kMask33) <= p.cap_chunks * (unsigned long long)kChunk);
+            DS_ASSERT(ldcg(&c->s_count[0]) <= (unsigned long long)p.n && ldcg(&c->s_count[1]) <= (unsigned long long)p.n);
+        }
+#endif
         if (p.trace && blockIdx.x == 0 && threadIdx.x == 0 && st < p.trace_cap) {
             p.trace[2 * st] = globaltimer_ns();
             p.trace[2 * st + 1] = (kind << 56) | (work & ((1ull << 56) - 1));
@@ -2151,6 +2217,7 @@ __global__ void __launch_bounds__(kThreads, DS_MIN_BLOCKS)
     auto wide_setup = [&](long long idx0, unsigned G) -> bool {
         const long long r0 = idx0 >> p.ksub_log2;
         const int wn = (int)(((idx0 + (long long)G - 1) >> p.ksub_log2) - r0 + 1);
+        DS_ASSERT(wn >= 1 && wn <= kWideRef);
         __syncthreads();
         if (threadIdx.x == 0) {
             sm.wn = wn;
