@@ -2135,12 +2135,26 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
         CK(cudaEventRecord(g->batch_ev, g->stream));
         for (int t = 0; t < T; ++t) CK(cudaStreamWaitEvent(ctx[t].stream, g->batch_ev, 0));
     }
-    const unsigned grid = T == 1 ? full_grid(g) : std::max(1u, full_grid(g) / (unsigned)T);
     const long long n = g->n;
+    // Passes: sources whose solve raised a fixed-point overflow or left the lex
+    // key range are collected and solved again AS A BATCH after the handle is
+    // re-prepared for them (binary64 / the reference's schedule) -- a graph
+    // whose every source fails that way costs one wasted pass, not a
+    // sequential tail.  `order` lists the source indices of the current pass.
+    std::vector<long long> order((size_t)k);
+    for (long long i = 0; i < k; ++i) order[(size_t)i] = i;
+    std::vector<char> overflowed((size_t)k, 0);
+    std::vector<std::vector<std::pair<long long, int>>> redo(T);  // (source index, device status)
+    for (int pass = 0; pass < 3 && !order.empty(); ++pass) {
+    if (pass > 0) {
+        if ((rc = prepare(g, delta, flags))) return rc;
+        for (auto& r : redo) r.clear();
+    }
+    const long long todo = (long long)order.size();
+    const unsigned grid = T == 1 ? full_grid(g) : std::max(1u, full_grid(g) / (unsigned)T);
     std::atomic<long long> next(0);
     std::vector<int> err(T, DS_OK);
     std::vector<std::string> msg(T);
-    std::vector<std::vector<std::pair<long long, int>>> redo(T);  // (source index, device status)
     auto worker = [&](int t) {
         cudaSetDevice(g->device);
         SolveCtx& x = ctx[t];
@@ -2188,8 +2202,9 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
             return r;
         };
         for (long long j = 0;; ++j) {
-            const long long i = next.fetch_add(1);
-            if (i >= k) break;
+            const long long qi = next.fetch_add(1);
+            if (qi >= todo) break;
+            const long long i = order[(size_t)qi];
             const int v = (int)(j & 1);
             if (zc_dev) {
                 xv[v].out = zc_dev + i * n;  // the finalize writes the caller's row
@@ -2199,7 +2214,7 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
                 if (j >= 2 && cudaStreamWaitEvent(x.stream, x.copied[v], 0) != cudaSuccess) {
                     err[t] = set_err(DS_ECUDA, "CUDA error ordering a batch output buffer");
                     msg[t] = g_err;
-                    next.store(k);
+                    next.store(todo);
                     break;
                 }
             }
@@ -2211,7 +2226,7 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
             if (r != DS_OK) {
                 err[t] = r;
                 msg[t] = g_err;
-                next.store(k);  // stop the other workers after their current source
+                next.store(todo);  // stop the other workers after their current source
                 break;
             }
         }
@@ -2240,6 +2255,32 @@ extern "C" int ds_sssp_batch(ds_graph* g, const int64_t* sources, int64_t k, dou
     }
     for (int t = 0; t < T; ++t)
         if (err[t] != DS_OK) return set_err(err[t], "%s", msg[t].c_str());
+    // the next pass: everything that failed, with the handle switched over
+    order.clear();
+    bool any_lex = false, any_ovf = false;
+    for (int t = 0; t < T; ++t)
+        for (const auto& [i, why] : redo[t]) {
+            order.push_back(i);
+            if (why == kDevOverflow) {
+                any_ovf = true;
+                overflowed[(size_t)i] = 1;
+            } else {
+                any_lex = true;
+            }
+        }
+    if (pass == 2 || order.empty()) break;  // (a third failure is left to the single-solve path below)
+    if (any_lex) {
+        if (delta == g->lexfail_delta && !any_ovf) break;
+        g->lexfail_delta = delta;
+    }
+    if (any_ovf) {
+        if (delta == g->overflow_delta) break;
+        g->overflow_delta = delta;
+    }
+    }  // passes
+    if (stats)
+        for (long long i = 0; i < k; ++i)
+            if (overflowed[(size_t)i]) stats[i].fallbacks = 1;  // its fixed-point solve overflowed in the batch
     // the handle's stream continues after every context's work
     for (int t = 0; t < T && T > 1; ++t) {
         cudaEvent_t e = t == 0 ? g->batch_ev : ctx[t].ready;

@@ -176,3 +176,30 @@ def test_bidirectional_entry(bidir_mode):
     b = graphs.rmat(12, seed=9, weight_seed=1)
     for s in graphs.pick_sources(b.indptr, 4, seed=5):
         _check(b, int(s), 0.3)
+
+
+def test_batch_lex_range_failure_reruns_as_a_batch():
+    """fp32-lattice weights with distances beyond the key range (D >= 2^26 at 24
+    fractional bits, i.e. >= 4.0): every lex solve of the batch raises the range
+    flag, the handle switches to the reference's schedule and the failed sources
+    run again as a batch -- same results as single solves and the oracle."""
+    # a path graph with weights near 0.5: the far end lies at ~32
+    n = 64
+    rng = np.random.default_rng(3)
+    w = (np.floor((0.5 + 0.25 * rng.random(n - 1)) * (1 << 24)) / (1 << 24))
+    edges = []
+    for i in range(n - 1):
+        edges.append((i, i + 1, w[i]))
+        edges.append((i + 1, i, w[i]))
+    from paper_1911_06895_b200 import matrix_build
+    a = matrix_build(n, np.array(edges))
+    g = DeviceGraph.from_matrix(a)
+    try:
+        srcs = [0, 5, 17, 40, 63]
+        stats, dist = g.solve_batch(srcs, 0.3, concurrency=3)
+        for i, s in enumerate(srcs):
+            want, outer, phases = oracle.delta_stepping(a.n, a.indptr, a.col, a.val, s, 0.3, threads=2)
+            assert np.array_equal(_bits(dist[i]), _bits(want)), s
+            assert (stats[i].outer_iterations, stats[i].inner_phases) == (outer, phases), s
+    finally:
+        g.close()
