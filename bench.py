@@ -671,7 +671,9 @@ def main():
 
         A = SparseMatrix(n, indptr_h, col_h.astype(np.int64), val_h.astype(np.float64))
         clear_device_cache()
-        delta_stepping_batch(A, batch(0)[:2], delta, concurrency=conc)  # warm
+        # warm: one full batch, so the drop-in's pooled pinned host buffers exist
+        # (they persist across calls; the device cache does not)
+        delta_stepping_batch(A, batch(0), delta, concurrency=conc)
         clear_device_cache()
         barrier()
         t0 = time.perf_counter()

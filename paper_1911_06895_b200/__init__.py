@@ -34,6 +34,7 @@ from .sssp import (  # noqa: F401
     SsspResult,
     bucket_bounds,
     clear_device_cache,
+    clear_host_buffers,
     delta_stepping,
     delta_stepping_batch,
     split_edges,
@@ -52,6 +53,7 @@ __all__ = [
     "SsspResult",
     "bucket_bounds",
     "clear_device_cache",
+    "clear_host_buffers",
     "delta_stepping",
     "delta_stepping_batch",
     "split_edges",

@@ -29,7 +29,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import _lib
+from . import _hostio, _lib
 from .containers import SparseMatrix, SparseVector
 
 __all__ = [
@@ -173,10 +173,34 @@ class DeviceGraph:
             if val.dtype not in (np.float32, np.float64, np.int32):
                 val = val.astype(np.float64)
         nnz = int(col.shape[0])
+        # Large pageable host arrays (the reference's int64 / float64 layout)
+        # go up through the pinned ring (_hostio): ~4x the pageable copy rate.
+        staged = []
+        host = [a for a in (indptr, col, val) if not hasattr(a, "data_ptr")]
+        if host and sum(a.nbytes for a in host) >= _hostio.MIN_BYTES and _hostio.available():
+            import torch
+
+            free, _ = torch.cuda.mem_get_info(device)
+            if 3 * sum(a.nbytes for a in host) < free:
+                def up(a):
+                    if hasattr(a, "data_ptr") or a.nbytes < _hostio.MIN_BYTES:
+                        return a
+                    t = _hostio.upload(a, device)
+                    staged.append(t)
+                    return t
+
+                indptr, col, val = up(indptr), up(col), up(val)
         h = ctypes.c_void_p()
-        _lib.check(L.ds_graph_create(int(n), nnz, _ptr(indptr), _ptr(col), _col_dtype(dt(col)),
-                                     _ptr(val), _val_dtype(dt(val)), int(device), stream or 0,
-                                     ctypes.byref(h)))
+        try:
+            _lib.check(L.ds_graph_create(int(n), nnz, _ptr(indptr), _ptr(col), _col_dtype(dt(col)),
+                                         _ptr(val), _val_dtype(dt(val)), int(device), stream or 0,
+                                         ctypes.byref(h)))
+        finally:
+            if staged:
+                import torch
+
+                del staged[:], indptr, col, val
+                torch.cuda.empty_cache()  # the staging copies go back to the driver
         return cls(h.value, n, nnz, device)
 
     @classmethod
@@ -342,6 +366,12 @@ def _retire(g: DeviceGraph) -> None:
         g.close()
 
 
+def clear_host_buffers() -> None:
+    """Release the pooled pinned host buffers of the drop-in entry points
+    (kept across calls: pinning 8 GB costs more than moving it)."""
+    _hostio.clear()
+
+
 def clear_device_cache() -> None:
     with _CACHE_LOCK:
         for _, g in _CACHE.values():
@@ -441,21 +471,44 @@ def delta_stepping_batch(
     if not srcs:
         return []
     start = time.perf_counter()
-    with _device_graph(matrix) as g:
-        stats, dist = g.solve_batch(srcs, float(delta), skip_empty_buckets=skip_empty_buckets,
-                                    concurrency=concurrency)
-    # dense rows -> reached (index, value) pairs; numpy releases the GIL on
-    # these full-row passes, so rows convert in parallel
-    def sparse_row(i):
-        row = dist[i]
-        idx = np.flatnonzero(row != np.inf)
-        return idx, row[idx]
+    # the dense results land in a pooled pinned array (no freshly faulted
+    # pages, full-rate D2H); the rows are copied out of it below
+    pooled = None
+    out = dist = None
+    nbytes = len(srcs) * matrix.n * 8
+    if nbytes >= _hostio.MIN_BYTES and _hostio.available():
+        pooled = _hostio.take_pinned(nbytes)
+        out = pooled.numpy()[:nbytes].view(np.float64).reshape(len(srcs), matrix.n)
+    try:
+        with _device_graph(matrix) as g:
+            stats, dist = g.solve_batch(srcs, float(delta), skip_empty_buckets=skip_empty_buckets,
+                                        concurrency=concurrency, out=out)
+        # dense rows -> reached (index, value) pairs; numpy releases the GIL on
+        # these full-row passes, so rows convert in parallel.  Sources of one
+        # component reach the same set: a row with as many reached vertices as
+        # the first one, all of them finite on its index set, shares that set.
+        first = np.flatnonzero(dist[0] != np.inf)
 
-    if len(srcs) > 1 and matrix.n >= (1 << 16):
-        with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1, 16)) as ex:
-            rows = list(ex.map(sparse_row, range(len(srcs))))
-    else:
-        rows = [sparse_row(i) for i in range(len(srcs))]
+        def sparse_row(i):
+            row = dist[i]
+            if i == 0:
+                return first, row[first]
+            if int(stats[i].reached) == first.size:
+                vals = row[first]
+                if not np.isinf(vals).any():
+                    return first, vals
+            idx = np.flatnonzero(row != np.inf)
+            return idx, row[idx]
+
+        if len(srcs) > 1 and matrix.n >= (1 << 16):
+            with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1, 16)) as ex:
+                rows = list(ex.map(sparse_row, range(len(srcs))))
+        else:
+            rows = [sparse_row(i) for i in range(len(srcs))]
+    finally:
+        if pooled is not None:
+            out = dist = None  # views of the pooled buffer
+            _hostio.give_pinned(pooled)
     elapsed = (time.perf_counter() - start) / len(srcs)
     out = []
     for (idx, val), st in zip(rows, stats):
