@@ -22,6 +22,7 @@ _CHUNK = 64 << 20  # upload ring chunk
 _PARTS = 8  # host threads per chunk copy
 _COPIERS = ThreadPoolExecutor(max_workers=_PARTS, thread_name_prefix="ds-hostio")
 MIN_BYTES = 64 << 20  # below this the plain path is as fast
+MAX_POOLED = 16 << 30  # largest result array taken from the pool (pinning more starves the host)
 
 
 def available() -> bool:

@@ -476,9 +476,12 @@ def delta_stepping_batch(
     pooled = None
     out = dist = None
     nbytes = len(srcs) * matrix.n * 8
-    if nbytes >= _hostio.MIN_BYTES and _hostio.available():
-        pooled = _hostio.take_pinned(nbytes)
-        out = pooled.numpy()[:nbytes].view(np.float64).reshape(len(srcs), matrix.n)
+    if _hostio.MIN_BYTES <= nbytes <= _hostio.MAX_POOLED and _hostio.available():
+        try:
+            pooled = _hostio.take_pinned(nbytes)
+            out = pooled.numpy()[:nbytes].view(np.float64).reshape(len(srcs), matrix.n)
+        except RuntimeError:  # no pinned memory to be had: the plain pageable result array
+            pooled = out = None
     try:
         with _device_graph(matrix) as g:
             stats, dist = g.solve_batch(srcs, float(delta), skip_empty_buckets=skip_empty_buckets,
