@@ -35,10 +35,19 @@
 //            shared-memory slice, maps each edge to its row, then issues
 //            lane-strided (coalesced) edge loads, the distance loads and the
 //            atomicMin pushes as three batched latency stages.
-//  Dedup of the next frontier and of S uses 1 bit per vertex (L2-resident
-//  bitmaps), cleared by the step that consumes the list.  Appends are staged
-//  in the warp's shared-memory queue (ballot prefix) and flushed with one
-//  global atomic per chunk.
+//  Dedup of the next frontier uses 1 bit per vertex (an L2-resident bitmap),
+//  cleared by the step that consumes the list; S needs none in the push builds
+//  (the one push that brings a vertex into the window tags its entry).  Appends
+//  are staged in the warp's shared-memory queue (ballot prefix) and flushed
+//  with one global atomic per chunk.
+//
+// Schedules.  Binary64 graphs run exactly the reference's bucket / phase
+// schedule above.  Fixed-point graphs run the "lex" schedule (see "lex mode"):
+// distance words carry a hop count, from which the reference's counters are
+// recovered whatever the processing order -- ksub internal buckets per
+// reference bucket while the buckets are large, then (see "wide windows" and
+// "bidirectional step") the latency-bound tail as one label-correcting
+// closure over every edge of the frontier rows.
 #pragma once
 
 #include <cooperative_groups.h>
